@@ -1,0 +1,435 @@
+"""Benchmark: BASELINE metric "ball x sensor pair-evals/s (fwd+adjoint) and
+iteration ms" on BASELINE config 2 (default; `--config` selects others).
+
+One step = one full 4D iteration through the fused engine: deform ->
+forward + residual + L2 loss -> adjoint -> deformation backward ->
+[NCCL all-reduce] -> finite guard + the iteration's single host sync ->
+Adam/floors.  value = B*M*F pair-evals of the whole job per second of step
+time (max over ranks).  Inputs are seeded synthetic scenes
+(paper_2412_03898_b200.synth); L2 is flushed (a 256 MiB write) between timed
+steps, outside each step's CUDA-event bracket.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C]
+    python bench.py --impl reference ...   # CPU oracle port, host threads
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ball x sensor pair-evals/s (fwd+adjoint), full 4D iteration"
+UNIT = "pair-evals/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
+FLOPS_PER_SAMPLE = 20.0     # fwd 7 + adj 13 canonical flops
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sensors", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def sm_peak_fp32():
+    """FP32 FMA peak: 148 SMs x 128 lanes x 2 flop x max SM clock."""
+    mhz = 1965.0
+    src = "derived: 148 SM x 128 FP32 lanes x 2 flop x 1965 MHz (sm_max_mhz)"
+    if PEAKS.exists():
+        try:
+            mhz = float(json.loads(PEAKS.read_text()).get("sm_max_mhz", mhz))
+            src = (f"derived: 148 SM x 128 FP32 lanes x 2 flop x {mhz:.0f} MHz"
+                   f" (MEASURED_PEAKS.json sm_max_mhz)")
+        except Exception:
+            pass
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12, src
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,"
+         "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/pacloud_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def support_samples_torch(mu_t, a0_t, pos, v, t0, dt, T, support=6.0):
+    """Exact in-support sample count (radiator.py:103-110) on the device,
+    as measurement plumbing (torch), frame by frame."""
+    import torch
+    total = 0
+    for f in range(mu_t.shape[0]):
+        for b0 in range(0, mu_t.shape[1], 65536):
+            mu = mu_t[f, b0:b0 + 65536]
+            a0 = a0_t[f, b0:b0 + 65536].double()
+            R = torch.cdist(mu, pos)                       # (b, M) f64
+            sa = support * a0[:, None]
+            lo = torch.ceil(((R - sa) / v - t0) / dt).clamp(0, T)
+            hi = (torch.floor(((R + sa) / v - t0) / dt) + 1).clamp(0, T)
+            total += int((hi - lo).clamp_min(0).sum().item())
+    return total
+
+
+def cpu_reference_sample(prob, n_sensors, threads):
+    """Oracle fwd+adjoint on a bounded sample: frame 0 (deformed states),
+    every k-th sensor, all balls.  Returns (pair-evals/s, desc, cores)."""
+    import oracle
+    from paper_2412_03898_b200.core import SensorArray
+    cfg = prob.config
+    st = oracle.cloud_states_at(prob.cloud, float(prob.frame_times[0]),
+                                cfg.coord_mode, cfg.a0_floor,
+                                basis=prob.cloud.basis)
+    M = prob.array.n_sensors
+    step = max(1, M // max(1, n_sensors))
+    sel = np.arange(0, M, step)[:n_sensors]
+    sub = SensorArray(prob.array.positions[sel], prob.array.sound_speed,
+                      prob.array.sample_rate, prob.array.n_samples,
+                      prob.array.t_start)
+    a, p, m = prob.gt_frames[0]
+    obs = oracle.forward_frame(oracle.States(a, p, m), sub, threads=threads)
+    oracle.forward_frame(st, sub, threads=threads)      # warm caches
+    best = math.inf
+    for _ in range(2):
+        t = time.perf_counter()
+        pred = oracle.forward_frame(st, sub, threads=threads)
+        oracle.frame_state_grads(st, sub, pred - obs, threads=threads)
+        best = min(best, time.perf_counter() - t)
+    pairs = len(st.a0_t) * len(sel)
+    desc = (f"frame 0, {len(sel)} of {M} sensors (every {step}th), all "
+            f"{len(st.a0_t)} balls; oracle fwd+adjoint fp64, min of 2")
+    return pairs / best, desc, best
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU port (the reference
+    is pure Python/numba; its C restatement in oracle/ is timed)."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2412_03898_b200 import synth
+    prob = synth.make_problem(args.config, seed=args.seed)
+    threads = os.cpu_count() or 1
+    n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
+    vals = []
+    desc = ""
+    for _ in range(max(1, args.warmup)):
+        cpu_reference_sample(prob, n_s, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, desc, _ = cpu_reference_sample(prob, n_s, threads)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = float(np.median(vals))
+    shp = prob.meta["shape"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * shp["B"] * shp["M"] * shp["F"] / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, fp32-quantised)",
+        "config": workload_config(args.config, prob, world),
+        "cpu_baseline": {"value": value, "unit": UNIT,
+                         "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg_id, prob, world):
+    shp = prob.meta["shape"]
+    shard = "sensors" if cfg_id == 4 else "frames"
+    return {"workload": f"BASELINE config {cfg_id}",
+            "balls": shp["B"], "sensors": shp["M"], "samples": shp["T"],
+            "frames": shp["F"], "basis": prob.cloud.basis,
+            "n_basis": int(prob.cloud.n_basis),
+            "coord_mode": prob.config.coord_mode,
+            "parallelism": f"{shard}-sharded x{world}" if world > 1
+            else "single GPU",
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2412_03898_b200 import _lib, synth
+    from paper_2412_03898_b200.engine import IterationEngine, shard_range
+    from paper_2412_03898_b200.radiator import DeviceArray, forward_device
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import datetime
+        torch.distributed.init_process_group(
+            "nccl", device_id=dev, timeout=datetime.timedelta(minutes=10))
+    prob = synth.make_problem(args.config, seed=args.seed)
+    shp = prob.meta["shape"]
+    B, M, T, F = shp["B"], shp["M"], shp["T"], shp["F"]
+    arr = prob.array
+    cfg = prob.config
+
+    # ---- observed traces: forward-simulate the ground-truth frames on the
+    # device (input synthesis, not timed; simulate_dataset geometry.py:266)
+    darr_full = DeviceArray(arr, cfg.support_sigmas, cfg.exact_forward)
+    obs = torch.empty((F, M, T), dtype=torch.float32, device=dev)
+    for k, (a, p, m) in enumerate(prob.gt_frames):
+        o, _, _ = forward_device(
+            darr_full, torch.as_tensor(m, device=dev).view(1, B, 3),
+            torch.as_tensor(a, dtype=torch.float32, device=dev).view(1, B),
+            torch.as_tensor(p, dtype=torch.float32, device=dev).view(1, B))
+        obs[k] = o[0]
+    del darr_full
+
+    sensor_shard = args.config == 4 and world > 1
+    frames_all = np.arange(F)
+    if sensor_shard:
+        lo, hi = shard_range(M, rank, world)
+        eng = IterationEngine(prob.cloud, arr, obs[:, lo:hi].contiguous(),
+                              prob.frame_times, cfg, sensors=(lo, hi))
+        local_frames = frames_all
+    else:
+        lo, hi = shard_range(F, rank, world)
+        local_frames = frames_all[lo:hi]
+        eng = IterationEngine(prob.cloud, arr, obs, prob.frame_times, cfg,
+                              frames=local_frames if world > 1 else None)
+    del obs
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    it = 0
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        eng.iterate(it, frames_all)
+        it += 1
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-step CUDA events, L2 flushed between
+    ev = [(torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record()
+            eng.iterate(it, frames_all)
+            ev[k][1].record()
+            it += 1
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    pairs = B * M * F
+    value = pairs / (ms * 1e-3)
+
+    # ---- dominant kernels: fwd + adj, timed live with events on the
+    # launching stream (eager, same buffers), and exact algorithmic work
+    F_loc = len(local_frames)
+    idx = np.arange(F_loc) if not sensor_shard else frames_all
+    eng.t_dev.copy_(torch.as_tensor(prob.frame_times[local_frames]))
+    from paper_2412_03898_b200.deformation import deform_states_device
+    from paper_2412_03898_b200.radiator import state_grads_device
+    deform_states_device(eng.dcloud, eng.t_dev, cfg.coord_mode, cfg.a0_floor,
+                         eng.mu_t, eng.a0_t, eng.p0_t, eng.H)
+    obs_loc = eng.observed[int(local_frames[0]):int(local_frames[0]) + F_loc] \
+        if not sensor_shard else eng.observed
+    reps = 5
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_fwd = t_adj = 0.0
+    for r in range(reps + 1):
+        flush.zero_()
+        e[0].record()
+        forward_device(eng.darr, eng.mu_t, eng.a0_t, eng.p0_t, observed=obs_loc,
+                       out=eng.resid, loss=eng.loss_f, coincident=eng.coinc,
+                       workspace=eng.ws)
+        e[1].record()
+        state_grads_device(eng.darr, eng.mu_t, eng.a0_t, eng.p0_t, eng.resid,
+                           G=eng.G, coincident=eng.coinc)
+        e[2].record()
+        torch.cuda.synchronize()
+        if r:
+            t_fwd += e[0].elapsed_time(e[1]) / reps
+            t_adj += e[1].elapsed_time(e[2]) / reps
+    S = support_samples_torch(eng.mu_t, eng.a0_t, eng.darr.positions,
+                              eng.darr.v, eng.darr.t0, eng.darr.dt,
+                              eng.darr.T, cfg.support_sigmas)
+    peak, peak_src = sm_peak_fp32()
+    achieved = FLOPS_PER_SAMPLE * S / ((t_fwd + t_adj) * 1e-3) / 1e12
+    traffic = None
+    if NCU_SUMMARY.exists():
+        try:
+            summ = json.loads(NCU_SUMMARY.read_text())
+            traffic = summ.get(f"config{args.config}", {}).get(
+                "dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    kern_pairs = B * eng.darr.M * F_loc
+    roofline = {
+        "bound": "fp32", "unit": "TFLOP/s", "achieved": achieved,
+        "peak": peak, "frac": achieved / peak, "traffic": traffic,
+        "kernel": "k_forward + k_adjoint (fwd+adj per local shard)",
+        "flops_per_launch": FLOPS_PER_SAMPLE * S,
+        "support_samples": S, "t_fwd_ms": t_fwd, "t_adj_ms": t_adj,
+        "kernel_pair_evals_per_s": kern_pairs / ((t_fwd + t_adj) * 1e-3),
+        "mufu_frac": 2.0 * S / ((t_fwd + t_adj) * 1e-3) /
+        (148 * 16 * 1965e6),
+        "peak_source": peak_src,
+    }
+
+    # ---- e2e: the user-facing call with host buffers (pinned observed in,
+    # loss out), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host_obs = eng.observed.cpu().pin_memory()
+        h2d = host_obs.numel() * host_obs.element_size()
+        barrier()
+        torch.cuda.synchronize()
+        ee = [(torch.cuda.Event(enable_timing=True),
+               torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        losses = []
+        for k in range(args.steps):
+            flush.zero_()
+            ee[k][0].record()
+            eng.observed.copy_(host_obs, non_blocking=True)
+            losses.append(eng.iterate(it, frames_all))   # D2H of the loss
+            ee[k][1].record()
+            it += 1
+        torch.cuda.synchronize()
+        ems = float(np.mean([a.elapsed_time(b) for a, b in ee]))
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": pairs / (ems * 1e-3), "unit": UNIT,
+               "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 8 + 4 * len(eng.layout.segments) + 8,
+               "api": "IterationEngine.iterate with observed copied from "
+                      "pinned host memory each step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
+        v, desc, secs = cpu_reference_sample(prob, n_s, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": desc}
+
+    # deform + forward[+combine]+loss-reduce + adjoint + deform-bwd + finite
+    # guard + Adam
+    launches_per_step = 5 + eng.darr.plan(B, F_loc)["launches"]
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded, fp32-quantised; observed traces "
+                    "forward-simulated from ground-truth frames)",
+            "config": workload_config(args.config, prob, world),
+            "iteration_ms": ms, "step_ms_min": float(np.min(step_ms)),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+            "final_loss": float(eng.loss_total.item()),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,221 @@
+/*
+ * pacloud_b200 -- C ABI of the B200 (sm_100a) hot path of 4D SlingBAG.
+ *
+ * Every entry point takes plain device pointers and sizes, is asynchronous on
+ * the caller's CUDA stream (`pc_stream_t` is a cudaStream_t; NULL = legacy
+ * default stream), allocates nothing persistent, and returns PC_OK or a
+ * nonzero status (argument error / CUDA launch error).  Data errors travel
+ * through device flag words that the host reads with the loss, once per
+ * iteration.  Each function cites the reference (read-only, pkg/src/pacloud)
+ * interface it replaces; the host-side mirror of the reference's Python
+ * signatures lives in paper_2412_03898_b200/ and INTEGRATION.md shows the
+ * ctypes binding a maintainer would add to the reference.
+ *
+ * Layouts (row-major, frame-major):
+ *   ball states   mu_t (F,B,3) f64, a0_t (F,B) f32, p0_t (F,B) f32
+ *   traces        (F,M,T) f32           (SignalSet.data is (M,K,T) upstream)
+ *   state grads   G (F,B,5) f32 in state order (a0, p0, mu_x, mu_y, mu_z)
+ *   parameters    f64 master copies; gradients f32; Adam moments f64
+ */
+#ifndef PACLOUD_B200_H
+#define PACLOUD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *pc_stream_t;
+
+#define PC_OK 0
+#define PC_ERR_ARGUMENT 1
+#define PC_ERR_CUDA 2
+#define PC_ERR_UNSUPPORTED 3
+
+/* coord_mode (core.py:21-24 COORD_MODES) */
+#define PC_COORD_MULTIPLICATIVE 0
+#define PC_COORD_ADDITIVE 1
+#define PC_COORD_RADIAL 2
+
+/* basis_kind: reference Gaussian basis (deformation.py:57-99) or the
+ * builder-defined cubic-polynomial + Fourier basis of BASELINE configs 2-5 */
+#define PC_BASIS_GAUSS 0
+#define PC_BASIS_POLYFOURIER 1
+
+/* SensorArray (core.py:295-354) plus the radiator knobs
+ * (radiator.py:195-197: support_sigmas, exact). */
+typedef struct pc_array {
+    const double *positions; /* device, (M,3) mm */
+    int32_t n_sensors;       /* M */
+    int32_t n_samples;       /* T */
+    double sound_speed;      /* mm/us */
+    double t_start;          /* us */
+    double dt;               /* us, 1/sample_rate (core.py:345-347) */
+    double support_sigmas;   /* radiator.py:31 DEFAULT_SUPPORT_SIGMAS */
+    int32_t exact;           /* evaluate every sample (radiator.py:100-102) */
+    int32_t reserved;
+} pc_array_t;
+
+/* DynamicCloud (core.py:166-259), device f64 arrays.
+ * Gaussian basis: theta/sigma (B,N) shared or (B,5,N) per-channel.
+ * Poly+Fourier basis: theta/sigma unused (may be NULL), N = 4 + 2*harmonics. */
+typedef struct pc_cloud {
+    const double *p0;    /* (B,)   */
+    const double *a0;    /* (B,)   */
+    const double *mu;    /* (B,3)  */
+    const double *theta; /* (B,N) or (B,5,N) */
+    const double *sigma; /* same shape as theta */
+    const double *omega; /* (B,5,N) */
+    int64_t n_balls;
+    int32_t n_basis;
+    int32_t per_channel; /* theta/sigma are (B,5,N) */
+    int32_t basis_kind;  /* PC_BASIS_* */
+    int32_t reserved;
+} pc_cloud_t;
+
+/* Parameter-gradient outputs (radiator.py:245-263 CloudGrads), device f32. */
+typedef struct pc_cloud_grads {
+    float *p0;    /* (B,)  */
+    float *a0;    /* (B,)  */
+    float *mu;    /* (B,3) */
+    float *theta; /* like cloud.theta (unused for poly+Fourier) */
+    float *sigma;
+    float *omega; /* (B,5,N) */
+} pc_cloud_grads_t;
+
+/* ---- deformation ------------------------------------------------------ */
+
+/* Replaces deformation.py:184-204 cloud_states_at, batched over F frames
+ * (the reference calls it once per frame, reconstruction.py:305).
+ * a0_floor <= 0 disables the clamp (a0_floor=None).  H (F,B,5) f32 receives
+ * the channel sums for pc_deform_backward (may be NULL). */
+int pc_deform_states(const pc_cloud_t *cloud, const double *t_frames_dev,
+                     int32_t n_frames, int32_t coord_mode, double a0_floor,
+                     double *mu_t, float *a0_t, float *p0_t, float *H,
+                     pc_stream_t stream);
+
+/* Replaces deformation.py:219-267 cloud_state_grads at one frame time
+ * (materialised Jacobians, f64; API compatibility -- the fused engine never
+ * materialises them). */
+int pc_deform_jacobian(const pc_cloud_t *cloud, double t, int32_t coord_mode,
+                       double a0_floor, double *d_base, double *d_omega,
+                       double *d_theta, double *d_sigma, pc_stream_t stream);
+
+/* Replaces radiator.py:278-294 (accumulate_frame_grads' chain rule) for one
+ * frame: G (B,5) f32 through a materialised Jacobian bundle into f64 grads.
+ * omega_row: host int[5] (deformation.py:87-90); shared: theta is (B,N). */
+int pc_assemble_grads(const float *G, int64_t n_balls, int32_t n_basis,
+                      const double *d_base, const double *d_omega,
+                      const double *d_theta, const double *d_sigma,
+                      const int32_t *omega_row_host, int32_t shared,
+                      int32_t with_theta_sigma, double *g_p0, double *g_a0,
+                      double *g_mu, double *g_theta, double *g_sigma,
+                      double *g_omega, pc_stream_t stream);
+
+/* Fused deformation backward over F frames: the chain rule of
+ * radiator.py:278-294 through deformation.py:219-267, summed over frames as
+ * reconstruction.py:303-316 does, without materialising any Jacobian.
+ * G and H are (F,B,5) from pc_residual_state_grads / pc_deform_states.
+ * Gradients are overwritten. */
+int pc_deform_backward(const pc_cloud_t *cloud, const double *t_frames_dev,
+                       int32_t n_frames, int32_t coord_mode, double a0_floor,
+                       const float *G, const float *H,
+                       const pc_cloud_grads_t *grads, pc_stream_t stream);
+
+/* ---- radiator ---------------------------------------------------------- */
+
+/* Launch plan of pc_forward_traces for this problem: plan[0] = samples per
+ * shared-memory time segment, plan[1] = segments, plan[2] = ball chunks
+ * (> 1 adds a chunk-combine launch), plan[3] = kernel launches per call. */
+int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array_t *array,
+                    int32_t *plan);
+
+/* Scratch bytes pc_forward_traces needs for this problem (0 = none). */
+size_t pc_forward_workspace_bytes(int64_t n_balls, int32_t n_frames,
+                                  const pc_array_t *array);
+
+/* Replaces radiator.py:86-118 _forward_traces (+ forward_frame :195-216),
+ * batched over F frames, with the residual and L2 loss of
+ * reconstruction.py:312-313 fused: if `observed` (F,M,T) is non-NULL, `out`
+ * receives predicted - observed and loss_per_frame[f] = 0.5*sum r^2 (f64);
+ * otherwise `out` receives the predicted traces.  `out` is overwritten.
+ * coincident: device int64, must hold INT64_MAX on entry; receives the
+ * smallest b*M+m of any pair with R < 1e-9 (radiator.py:97-99). */
+int pc_forward_traces(const double *mu_t, const float *a0_t,
+                      const float *p0_t, int64_t n_balls, int32_t n_frames,
+                      const pc_array_t *array, const float *observed,
+                      float *out, double *loss_per_frame,
+                      int64_t *coincident, void *workspace,
+                      size_t workspace_bytes, pc_stream_t stream);
+
+/* Replaces radiator.py:121-174 _residual_state_grads (+ frame_state_grads
+ * :219-242), batched over F frames: G (F,B,5) f32 is overwritten with the
+ * gradient of 0.5*||residual||^2 w.r.t. (a0_t, p0_t, mu_t). */
+int pc_residual_state_grads(const double *mu_t, const float *a0_t,
+                            const float *p0_t, int64_t n_balls,
+                            int32_t n_frames, const pc_array_t *array,
+                            const float *residual, float *G,
+                            int64_t *coincident, pc_stream_t stream);
+
+/* ---- loss and optimiser ------------------------------------------------- */
+
+/* Replaces reconstruction.py:28-35 l2_loss: out[0] = 0.5*sum (p-o)^2 (f64,
+ * fixed-order reduction). */
+int pc_l2_loss(const double *predicted, const double *observed, int64_t n,
+               double *out, pc_stream_t stream);
+
+/* Non-finite scan (reconstruction.py:60-61): flags[s] |= 1 when segment s of
+ * x (f32) holds a NaN/Inf.  seg_off is a host array of n_seg+1 offsets. */
+int pc_check_finite(const float *x, int32_t n_seg, const int64_t *seg_off,
+                    int32_t *flags, pc_stream_t stream);
+
+/* Replaces reconstruction.py:57-69 adam_step (+ the floors of :153-157) for
+ * n_seg parameter segments of one flat buffer in one launch.  Per segment:
+ * learning rate, step count t (after increment) and lower floor
+ * (-inf = none).  seg_off / seg_lr / seg_step / seg_floor are host arrays;
+ * at most PC_MAX_SEGMENTS segments. */
+#define PC_MAX_SEGMENTS 16
+int pc_adam_segments(double *params, const float *grads, double *m,
+                     double *v, int32_t n_seg, const int64_t *seg_off,
+                     const double *seg_lr, const int32_t *seg_step,
+                     const double *seg_floor, pc_stream_t stream);
+
+/* Replaces reconstruction.py:72-76 sgd_step over segments. */
+int pc_sgd_segments(double *params, const float *grads, int32_t n_seg,
+                    const int64_t *seg_off, const double *seg_lr,
+                    const double *seg_floor, pc_stream_t stream);
+
+/* ---- prune / densify compaction ----------------------------------------- */
+
+/* Workspace bytes for pc_prune_mask / pc_compact_index on B balls. */
+size_t pc_compact_workspace_bytes(int64_t n_balls);
+
+/* reconstruction.py:217-220: keep[b] = p0[b] > rel_threshold*max(p0, 0);
+ * n_keep (device int64) receives the survivor count. */
+int pc_prune_mask(const double *p0, int64_t n_balls, double rel_threshold,
+                  uint8_t *keep, int64_t *n_keep, void *workspace,
+                  size_t workspace_bytes, pc_stream_t stream);
+
+/* Stable compaction order (reconstruction.py:95-100 boolean gather):
+ * index[0..n_keep) = ascending b with keep[b]; then, if `append` is non-NULL,
+ * index[n_keep..n_keep+n_append) = ascending b with append[b] (children of
+ * the config-5 split, appended after the survivors in parent order).
+ * n_out (device int64) = n_keep + n_append. */
+int pc_compact_index(const uint8_t *keep, const uint8_t *append,
+                     int64_t n_balls, int64_t *index, int64_t *n_out,
+                     void *workspace, size_t workspace_bytes,
+                     pc_stream_t stream);
+
+/* dst[i, :] = src[index[i], :] for i < n_rows (row_bytes a multiple of 4). */
+int pc_gather_rows(const void *src, void *dst, const int64_t *index,
+                   int64_t n_rows, int64_t row_bytes, pc_stream_t stream);
+
+/* Library version string (static). */
+const char *pc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PACLOUD_B200_H */

@@ -1,0 +1,34 @@
+"""B200-native hot path of 4D SlingBAG (arXiv 2412.03898).
+
+Drop-in replacements for the reference ``pacloud`` hot-path calls, backed by
+hand-written sm_100a CUDA kernels behind a C ABI (libpacloud_b200.so,
+include/pacloud_b200.h):
+
+    deformation.cloud_states_at / cloud_state_grads
+    radiator.forward_frame / frame_state_grads / accumulate_frame_grads
+    reconstruction.l2_loss / adam_step / sgd_step / ParamGroup(s) /
+        dynamic_reconstruct
+    engine.IterationEngine      fused multi-frame iteration (+ NCCL sharding)
+"""
+
+from .core import (AdamState, BallStateAtT, CloudGrads, CloudState,
+                   CloudStateGrad, DynamicCloud, ReconConfig, SensorArray,
+                   SignalSet, default_basis_grid, frame_times)
+from .deformation import cloud_state_grads, cloud_states_at
+from .engine import IterationEngine
+from .radiator import (accumulate_frame_grads, forward_frame,
+                       frame_state_grads)
+from .reconstruction import (ParamGroup, ParamGroups, adam_step,
+                             dynamic_reconstruct, l2_loss, scheduled_lr,
+                             sgd_step)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AdamState", "BallStateAtT", "CloudGrads", "CloudState", "CloudStateGrad",
+    "DynamicCloud", "ReconConfig", "SensorArray", "SignalSet",
+    "default_basis_grid", "frame_times", "cloud_state_grads",
+    "cloud_states_at", "IterationEngine", "accumulate_frame_grads",
+    "forward_frame", "frame_state_grads", "ParamGroup", "ParamGroups",
+    "adam_step", "dynamic_reconstruct", "l2_loss", "scheduled_lr", "sgd_step",
+]

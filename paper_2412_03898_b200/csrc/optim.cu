@@ -1,0 +1,369 @@
+// Loss, optimiser and compaction kernels (HBM-bound) for sm_100a.
+//
+//   pc_l2_loss          <- pkg/src/pacloud/reconstruction.py:28-35 (l2_loss)
+//   pc_check_finite     <- reconstruction.py:60-61, 74-75 (non-finite guard)
+//   pc_adam_segments    <- reconstruction.py:57-69 (adam_step) x the four
+//                          ParamGroups (:320-327) + _clamp_floors (:153-157)
+//   pc_sgd_segments     <- reconstruction.py:72-76 (sgd_step)
+//   pc_prune_mask       <- reconstruction.py:217-220 (keep = p0 > thr*max p0)
+//   pc_compact_index    <- reconstruction.py:95-100 (stable boolean gather)
+//   pc_gather_rows      <- the gather itself, for params and Adam moments
+#include <math.h>
+
+#include "common.cuh"
+
+namespace pc {
+
+// ---------------------------------------------------------------- l2 loss
+
+__global__ void __launch_bounds__(1024) k_l2(const double* __restrict__ p,
+                                             const double* __restrict__ o, int64_t n,
+                                             double* __restrict__ out) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double d = p[i] - o[i];
+        s = fma(d, d, s);
+    }
+    __shared__ double red[32];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) out[0] = 0.5 * t;
+    }
+}
+
+// ---------------------------------------------------------------- segments
+
+struct SegTable {
+    int64_t off[PC_MAX_SEGMENTS + 1];
+    double lr[PC_MAX_SEGMENTS];
+    double bc1[PC_MAX_SEGMENTS];
+    double bc2[PC_MAX_SEGMENTS];
+    double floor_[PC_MAX_SEGMENTS];
+    int n;
+};
+
+__global__ void __launch_bounds__(256) k_finite(const float* __restrict__ x, SegTable t,
+                                                int* __restrict__ flags) {
+    const int s = blockIdx.y;
+    const int64_t lo = t.off[s], hi = t.off[s + 1];
+    int bad = 0;
+    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    bad = __syncthreads_or(bad);
+    if (bad && threadIdx.x == 0) atomicOr(flags + s, 1);
+}
+
+constexpr double kBeta1 = 0.9, kBeta2 = 0.999, kEps = 1e-8;  // reconstruction.py:23-25
+
+__global__ void __launch_bounds__(256) k_adam(double* __restrict__ p, const float* __restrict__ g,
+                                              double* __restrict__ m, double* __restrict__ v,
+                                              SegTable t) {
+    const int s = blockIdx.y;
+    const int64_t lo = t.off[s], hi = t.off[s + 1];
+    const double lr = t.lr[s], bc1 = t.bc1[s], bc2 = t.bc2[s], fl = t.floor_[s];
+    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double gi = (double)g[i];
+        double mi = m[i] * kBeta1;
+        mi = mi + (1.0 - kBeta1) * gi;
+        double vi = v[i] * kBeta2;
+        vi = vi + (1.0 - kBeta2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        const double mh = mi / bc1;
+        const double vh = vi / bc2;
+        double pi = p[i] - lr * mh / (sqrt(vh) + kEps);
+        p[i] = pi < fl ? fl : pi;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sgd(double* __restrict__ p, const float* __restrict__ g,
+                                             SegTable t) {
+    const int s = blockIdx.y;
+    const int64_t lo = t.off[s], hi = t.off[s + 1];
+    const double lr = t.lr[s], fl = t.floor_[s];
+    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double pi = p[i] - lr * (double)g[i];
+        p[i] = pi < fl ? fl : pi;
+    }
+}
+
+static bool seg_table(int n_seg, const int64_t* off, SegTable& t) {
+    if (n_seg < 1 || n_seg > PC_MAX_SEGMENTS || !off) return false;
+    t.n = n_seg;
+    for (int s = 0; s <= n_seg; ++s) {
+        t.off[s] = off[s];
+        if (s > 0 && off[s] < off[s - 1]) return false;
+    }
+    if (off[0] < 0) return false;
+    return true;
+}
+
+static unsigned seg_blocks(const SegTable& t) {
+    int64_t widest = 0;
+    for (int s = 0; s < t.n; ++s) widest = t.off[s + 1] - t.off[s] > widest ? t.off[s + 1] - t.off[s] : widest;
+    int64_t b = (widest + 255) / 256;
+    const int64_t cap = 8LL * num_sms();
+    if (b > cap) b = cap;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------- compaction
+
+constexpr int CMP_BLOCK = 1024;
+
+__global__ void __launch_bounds__(1024) k_max(const double* __restrict__ x, int64_t n,
+                                              double* __restrict__ out) {
+    double mx = 0.0;  // np.max(p0, initial=0.0)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, x[i]);
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmax(t, red[w]);
+        out[0] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_prune(const double* __restrict__ p0, int64_t n, double rel,
+                                               const double* __restrict__ maxv,
+                                               uint8_t* __restrict__ keep,
+                                               unsigned long long* __restrict__ count) {
+    const double thr = rel * maxv[0];
+    int c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t k = p0[i] > thr ? 1 : 0;
+        keep[i] = k;
+        c += k;
+    }
+    c = __syncthreads_count(c);
+    if (threadIdx.x == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
+__global__ void __launch_bounds__(CMP_BLOCK) k_block_counts(const uint8_t* __restrict__ keep,
+                                                            const uint8_t* __restrict__ app,
+                                                            int64_t n, int64_t* __restrict__ ck,
+                                                            int64_t* __restrict__ ca) {
+    const int64_t i = (int64_t)blockIdx.x * CMP_BLOCK + threadIdx.x;
+    const int k = i < n && keep[i] ? 1 : 0;
+    const int a = i < n && app && app[i] ? 1 : 0;
+    const int sk = __syncthreads_count(k);
+    const int sa = __syncthreads_count(a);
+    if (threadIdx.x == 0) {
+        ck[blockIdx.x] = sk;
+        ca[blockIdx.x] = sa;
+    }
+}
+
+// exclusive scan of the per-block counts (single block, fixed order)
+__global__ void __launch_bounds__(1024) k_scan_counts(int64_t* __restrict__ ck,
+                                                      int64_t* __restrict__ ca, int nblk,
+                                                      int64_t* __restrict__ n_out) {
+    __shared__ int64_t sk[1024], sa[1024];
+    __shared__ int64_t carry_k, carry_a;
+    if (threadIdx.x == 0) carry_k = carry_a = 0;
+    __syncthreads();
+    for (int base = 0; base < nblk; base += 1024) {
+        const int i = base + threadIdx.x;
+        sk[threadIdx.x] = i < nblk ? ck[i] : 0;
+        sa[threadIdx.x] = i < nblk ? ca[i] : 0;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+            int64_t xk = threadIdx.x >= o ? sk[threadIdx.x - o] : 0;
+            int64_t xa = threadIdx.x >= o ? sa[threadIdx.x - o] : 0;
+            __syncthreads();
+            sk[threadIdx.x] += xk;
+            sa[threadIdx.x] += xa;
+            __syncthreads();
+        }
+        if (i < nblk) {
+            const int64_t ek = (threadIdx.x ? sk[threadIdx.x - 1] : 0) + carry_k;
+            const int64_t ea = (threadIdx.x ? sa[threadIdx.x - 1] : 0) + carry_a;
+            ck[i] = ek;
+            ca[i] = ea;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry_k += sk[1023];
+            carry_a += sa[1023];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        n_out[0] = carry_k + carry_a;
+        n_out[1] = carry_k;  // survivors (children start here)
+    }
+}
+
+__global__ void __launch_bounds__(CMP_BLOCK) k_scatter_index(const uint8_t* __restrict__ keep,
+                                                             const uint8_t* __restrict__ app,
+                                                             int64_t n,
+                                                             const int64_t* __restrict__ ck,
+                                                             const int64_t* __restrict__ ca,
+                                                             const int64_t* __restrict__ n_out,
+                                                             int64_t* __restrict__ index) {
+    __shared__ int wk[32], wa[32];
+    const int64_t i = (int64_t)blockIdx.x * CMP_BLOCK + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool k = i < n && keep[i];
+    const bool a = i < n && app && app[i];
+    const unsigned bk = __ballot_sync(0xffffffffu, k);
+    const unsigned ba = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) {
+        wk[warp] = __popc(bk);
+        wa[warp] = __popc(ba);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive scan over 32 warps
+        int rk = 0, ra = 0;
+        for (int w = 0; w < 32; ++w) {
+            const int tk = wk[w], ta = wa[w];
+            wk[w] = rk;
+            wa[w] = ra;
+            rk += tk;
+            ra += ta;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    if (k) index[ck[blockIdx.x] + wk[warp] + __popc(bk & lt)] = i;
+    if (a) index[n_out[1] + ca[blockIdx.x] + wa[warp] + __popc(ba & lt)] = i;
+}
+
+__global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ src,
+                                                uint32_t* __restrict__ dst,
+                                                const int64_t* __restrict__ index, int64_t rows,
+                                                int64_t words) {
+    const int64_t total = rows * words;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = q / words, w = q - r * words;
+        dst[q] = src[index[r] * words + w];
+    }
+}
+
+}  // namespace pc
+
+using namespace pc;
+
+extern "C" int pc_l2_loss(const double* predicted, const double* observed, int64_t n, double* out,
+                          pc_stream_t stream) {
+    if (n < 0 || !out || (n > 0 && (!predicted || !observed))) return PC_ERR_ARGUMENT;
+    k_l2<<<1, 1024, 0, as_stream(stream)>>>(predicted, observed, n, out);
+    return last_status();
+}
+
+extern "C" int pc_check_finite(const float* x, int32_t n_seg, const int64_t* seg_off,
+                               int32_t* flags, pc_stream_t stream) {
+    SegTable t;
+    if (!seg_table(n_seg, seg_off, t) || !flags) return PC_ERR_ARGUMENT;
+    if (t.off[n_seg] > t.off[0] && !x) return PC_ERR_ARGUMENT;
+    k_finite<<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(x, t, flags);
+    return last_status();
+}
+
+extern "C" int pc_adam_segments(double* params, const float* grads, double* m, double* v,
+                                int32_t n_seg, const int64_t* seg_off, const double* seg_lr,
+                                const int32_t* seg_step, const double* seg_floor,
+                                pc_stream_t stream) {
+    SegTable t;
+    if (!seg_table(n_seg, seg_off, t) || !seg_lr || !seg_step) return PC_ERR_ARGUMENT;
+    if (t.off[n_seg] > t.off[0] && (!params || !grads || !m || !v)) return PC_ERR_ARGUMENT;
+    for (int s = 0; s < n_seg; ++s) {
+        if (seg_step[s] < 1) return PC_ERR_ARGUMENT;
+        t.lr[s] = seg_lr[s];
+        t.bc1[s] = 1.0 - pow(kBeta1, (double)seg_step[s]);
+        t.bc2[s] = 1.0 - pow(kBeta2, (double)seg_step[s]);
+        t.floor_[s] = seg_floor ? seg_floor[s] : -INFINITY;
+    }
+    k_adam<<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(params, grads, m, v, t);
+    return last_status();
+}
+
+extern "C" int pc_sgd_segments(double* params, const float* grads, int32_t n_seg,
+                               const int64_t* seg_off, const double* seg_lr,
+                               const double* seg_floor, pc_stream_t stream) {
+    SegTable t;
+    if (!seg_table(n_seg, seg_off, t) || !seg_lr) return PC_ERR_ARGUMENT;
+    if (t.off[n_seg] > t.off[0] && (!params || !grads)) return PC_ERR_ARGUMENT;
+    for (int s = 0; s < n_seg; ++s) {
+        t.lr[s] = seg_lr[s];
+        t.floor_[s] = seg_floor ? seg_floor[s] : -INFINITY;
+        t.bc1[s] = t.bc2[s] = 1.0;
+    }
+    k_sgd<<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(params, grads, t);
+    return last_status();
+}
+
+extern "C" size_t pc_compact_workspace_bytes(int64_t n_balls) {
+    const int64_t nblk = (n_balls + CMP_BLOCK - 1) / CMP_BLOCK + 1;
+    return (size_t)(2 * nblk + 8) * sizeof(int64_t);
+}
+
+extern "C" int pc_prune_mask(const double* p0, int64_t n_balls, double rel_threshold,
+                             uint8_t* keep, int64_t* n_keep, void* workspace,
+                             size_t workspace_bytes, pc_stream_t stream) {
+    if (n_balls < 0 || !keep || !n_keep || !workspace || workspace_bytes < 16)
+        return PC_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(n_keep, 0, sizeof(int64_t), st) != cudaSuccess) return PC_ERR_CUDA;
+    if (n_balls == 0) return PC_OK;
+    if (!p0) return PC_ERR_ARGUMENT;
+    double* maxv = static_cast<double*>(workspace);
+    k_max<<<1, 1024, 0, st>>>(p0, n_balls, maxv);
+    int64_t blocks = (n_balls + 255) / 256;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    k_prune<<<(unsigned)blocks, 256, 0, st>>>(p0, n_balls, rel_threshold, maxv, keep,
+                                              reinterpret_cast<unsigned long long*>(n_keep));
+    return last_status();
+}
+
+extern "C" int pc_compact_index(const uint8_t* keep, const uint8_t* append, int64_t n_balls,
+                                int64_t* index, int64_t* n_out, void* workspace,
+                                size_t workspace_bytes, pc_stream_t stream) {
+    if (n_balls < 0 || !n_out || !workspace ||
+        workspace_bytes < pc_compact_workspace_bytes(n_balls))
+        return PC_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    if (n_balls == 0) {
+        return status_of(cudaMemsetAsync(n_out, 0, sizeof(int64_t), st));
+    }
+    if (!keep || !index) return PC_ERR_ARGUMENT;
+    const int64_t nblk = (n_balls + CMP_BLOCK - 1) / CMP_BLOCK;
+    int64_t* ck = static_cast<int64_t*>(workspace);
+    int64_t* ca = ck + nblk + 1;
+    int64_t* tot = ca + nblk + 1;  // [n_out, n_keep]
+    k_block_counts<<<(unsigned)nblk, CMP_BLOCK, 0, st>>>(keep, append, n_balls, ck, ca);
+    k_scan_counts<<<1, 1024, 0, st>>>(ck, ca, (int)nblk, tot);
+    k_scatter_index<<<(unsigned)nblk, CMP_BLOCK, 0, st>>>(keep, append, n_balls, ck, ca, tot,
+                                                          index);
+    if (cudaMemcpyAsync(n_out, tot, sizeof(int64_t), cudaMemcpyDeviceToDevice, st) !=
+        cudaSuccess)
+        return PC_ERR_CUDA;
+    return last_status();
+}
+
+extern "C" int pc_gather_rows(const void* src, void* dst, const int64_t* index, int64_t n_rows,
+                              int64_t row_bytes, pc_stream_t stream) {
+    if (n_rows < 0 || row_bytes < 0 || (row_bytes & 3)) return PC_ERR_ARGUMENT;
+    if (n_rows == 0 || row_bytes == 0) return PC_OK;
+    if (!src || !dst || !index) return PC_ERR_ARGUMENT;
+    const int64_t words = row_bytes / 4;
+    int64_t blocks = (n_rows * words + 255) / 256;
+    if (blocks > 16LL * num_sms()) blocks = 16LL * num_sms();
+    k_gather<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+        static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), index, n_rows, words);
+    return last_status();
+}
+
+extern "C" const char* pc_version(void) { return "pacloud_b200 0.1.0 (sm_100a)"; }

@@ -1,0 +1,390 @@
+"""Fused multi-frame 4D SlingBAG iteration on the B200 (one rank per GPU).
+
+One iteration of pkg/src/pacloud/reconstruction.py:293-328
+(``dynamic_reconstruct``'s loop body) as five device launches on one stream:
+
+    pc_deform_states        all selected frames at once      (deformation.py:184)
+    pc_forward_traces       fwd + residual + L2 loss          (radiator.py:86, reconstruction.py:312)
+    pc_residual_state_grads adjoint G (F,B,5)                 (radiator.py:121)
+    pc_deform_backward      chain rule summed over frames     (radiator.py:266, reconstruction.py:314)
+    pc_check_finite         non-finite guard per group        (reconstruction.py:60)
+
+then, for world_size > 1, one NCCL all-reduce of the flat float32 gradient
+buffer (+ the loss), ONE host synchronisation to read loss / flags, and one
+``pc_adam_segments`` launch covering all four parameter groups and the floors
+(reconstruction.py:320-328, :153-157).  The launch sequence up to the guard
+is captured once in a CUDA graph when the frame set is fixed.
+
+Parameters live in one flat float64 buffer (group order pressure, std,
+coords, deform -- the reference's update order), gradients in a float32
+buffer with the same offsets, Adam moments in float64.
+
+Sharding: ``frames`` restricts a rank to a subset of the
+selected frames (frame sharding); ``sensors=(lo, hi)`` restricts it to a
+sensor slice for every frame (sensor sharding; ball states are recomputed
+on every rank, i.e. broadcast).  Both end in the same gradient all-reduce.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import DynamicCloud, default_basis_grid
+from .deformation import (DeviceCloud, deform_backward_device,
+                          deform_states_device)
+from .radiator import (DeviceArray, forward_device, raise_if_coincident,
+                       state_grads_device, to_device)
+
+GROUP_ORDER = ("pressure", "std", "coords", "deform")
+GROUP_OF = {"p0": "pressure", "a0": "std", "mu": "coords", "theta": "deform",
+            "sigma": "deform", "omega": "deform"}
+
+
+def scheduled_lr(lr0, iteration, step_size, drop_rate):
+    """reconstruction.py:38-41."""
+    return lr0 * drop_rate ** (iteration // step_size)
+
+
+def select_frames(n_frames: int, batch: int, rng) -> np.ndarray:
+    """reconstruction.py:246-250 (same RNG draws as the reference)."""
+    if batch <= 0 or batch >= n_frames:
+        return np.arange(n_frames)
+    return np.sort(rng.choice(n_frames, size=batch, replace=False))
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of n items owned by `rank` of `world`."""
+    lo = (n * rank) // world
+    hi = (n * (rank + 1)) // world
+    return lo, hi
+
+
+@dataclass
+class Segment:
+    name: str
+    group: str
+    shape: tuple
+    offset: int
+    size: int
+
+
+class ParamLayout:
+    """Offsets of every parameter array inside the flat buffers."""
+
+    def __init__(self, B: int, N: int, basis: str, per_channel: bool):
+        shapes = [("p0", (B,)), ("a0", (B,)), ("mu", (B, 3))]
+        if basis == "gauss":
+            ts = (B, 5, N) if per_channel else (B, N)
+            shapes += [("theta", ts), ("sigma", ts)]
+        shapes += [("omega", (B, 5, N))]
+        self.segments = []
+        off = 0
+        for name, shp in shapes:
+            n = int(np.prod(shp))
+            self.segments.append(Segment(name, GROUP_OF[name], shp, off, n))
+            off += n
+        self.total = off
+        self.by_name = {s.name: s for s in self.segments}
+        self.offsets = [s.offset for s in self.segments] + [off]
+
+    def views(self, flat: torch.Tensor) -> dict:
+        return {s.name: flat[s.offset:s.offset + s.size].view(s.shape)
+                for s in self.segments}
+
+
+class IterationEngine:
+    """Device-resident parameters, Adam state and per-iteration buffers."""
+
+    def __init__(self, cloud, array, observed, frame_times, config, *,
+                 frames=None, sensors=None, process_group=None,
+                 use_graph=True, device=None):
+        _lib.load_library()
+        self.cfg = config
+        self.basis = getattr(cloud, "basis", getattr(config, "basis",
+                                                     "gauss"))
+        self.device = device or torch.device("cuda",
+                                             torch.cuda.current_device())
+        self.group = process_group
+        self.world = (torch.distributed.get_world_size(process_group)
+                      if process_group is not None
+                      or (torch.distributed.is_available()
+                          and torch.distributed.is_initialized()) else 1)
+        self.frame_times_all = np.asarray(frame_times, dtype=np.float64)
+        self.n_frames_all = len(self.frame_times_all)
+        self.local_frames = None if frames is None else np.asarray(frames)
+        lo, hi = sensors if sensors is not None else (0, array.n_sensors)
+        self.sensors = (int(lo), int(hi))
+        pos = np.asarray(array.positions)[lo:hi]
+        self.darr = DeviceArray(array, config.support_sigmas,
+                                config.exact_forward, positions=pos)
+        # observed: (F_all, M_local, T) float32 on the device
+        obs = observed
+        if not isinstance(obs, torch.Tensor):
+            obs = torch.as_tensor(np.ascontiguousarray(obs, np.float32))
+        if obs.shape[1] != self.darr.M:
+            obs = obs[:, lo:hi]
+        self.observed = obs.to(self.device, torch.float32).contiguous()
+        if tuple(self.observed.shape[1:]) != (self.darr.M, self.darr.T):
+            raise ValueError("observed must be (F, M, T) for this array")
+
+        # ---- flat parameter / gradient / moment buffers
+        B = len(cloud.p0)
+        N = int(np.asarray(cloud.omega).shape[-1]) if not isinstance(
+            cloud.omega, torch.Tensor) else int(cloud.omega.shape[-1])
+        per_channel = self.basis == "gauss" and np.ndim(cloud.theta) == 3
+        self.layout = ParamLayout(B, N, self.basis, per_channel)
+        self.B, self.N = B, N
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.P = torch.empty(self.layout.total, **f64)
+        self.Mo = torch.zeros(self.layout.total, **f64)
+        self.Vo = torch.zeros(self.layout.total, **f64)
+        self.Gf = torch.zeros(self.layout.total, dtype=torch.float32,
+                              device=self.device)
+        self.params = self.layout.views(self.P)
+        self.grads = self.layout.views(self.Gf)
+        for name in self.params:
+            src = getattr(cloud, name)
+            self.params[name].copy_(to_device(src, torch.float64)
+                                    .reshape(self.params[name].shape))
+        self.step_count = {s.name: 0 for s in self.layout.segments}
+        p = self.params
+        self.dcloud = DeviceCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
+                                  p.get("sigma"), p["omega"], self.basis)
+        self.use_graph = bool(use_graph)
+        self._graph = None
+        self._graph_frames = None
+        self._bufs_F = -1
+        n_seg = len(self.layout.segments)
+        self.flags = torch.zeros(n_seg, dtype=torch.int32, device=self.device)
+        self.coinc = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64,
+                                device=self.device)
+        self.loss_total = torch.zeros(1, dtype=torch.float64,
+                                      device=self.device)
+
+    # ------------------------------------------------------------ buffers
+    def _ensure_buffers(self, F: int):
+        if self._bufs_F == F:
+            return
+        dev, B, M, T = self.device, self.B, self.darr.M, self.darr.T
+        self.t_dev = torch.zeros(F, dtype=torch.float64, device=dev)
+        self.mu_t = torch.empty((F, B, 3), dtype=torch.float64, device=dev)
+        self.a0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
+        self.p0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
+        self.H = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
+        self.resid = torch.empty((F, M, T), dtype=torch.float32, device=dev)
+        self.G = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
+        self.loss_f = torch.zeros(F, dtype=torch.float64, device=dev)
+        ws = self.darr.workspace_bytes(max(B, 1), F)
+        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+        self.obs_stage = None
+        self._bufs_F = F
+        self._graph = None
+
+    def _local_frames(self, frames: np.ndarray) -> np.ndarray:
+        if self.local_frames is not None:
+            mine = set(int(k) for k in self.local_frames)
+            return np.array([k for k in frames if int(k) in mine],
+                            dtype=np.int64)
+        return frames
+
+    # ------------------------------------------------------------ compute
+    def _launch_compute(self, obs):
+        """deform -> forward+loss -> adjoint -> deformation backward."""
+        cfg = self.cfg
+        self.coinc.fill_(_lib.INT64_MAX)
+        deform_states_device(self.dcloud, self.t_dev, cfg.coord_mode,
+                             cfg.a0_floor, self.mu_t, self.a0_t, self.p0_t,
+                             self.H)
+        forward_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
+                       observed=obs, out=self.resid, loss=self.loss_f,
+                       coincident=self.coinc, workspace=self.ws)
+        state_grads_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
+                           self.resid, G=self.G, coincident=self.coinc)
+        deform_backward_device(self.dcloud, self.t_dev, cfg.coord_mode,
+                               cfg.a0_floor, self.G, self.H, self.grads)
+        torch.sum(self.loss_f, dim=0, keepdim=True, out=self.loss_total)
+
+    def compute_grads(self, frames: np.ndarray) -> None:
+        """Launch (asynchronously) the gradient of the selected frames."""
+        local = self._local_frames(np.asarray(frames))
+        F = len(local)
+        if F == 0:
+            self.Gf.zero_()
+            self.loss_total.zero_()
+            self.coinc.fill_(_lib.INT64_MAX)
+            return
+        self._ensure_buffers(F)
+        contiguous = np.array_equal(local, np.arange(local[0],
+                                                     local[0] + F))
+        if contiguous:
+            obs = self.observed[int(local[0]):int(local[0]) + F]
+        else:
+            if self.obs_stage is None:
+                self.obs_stage = torch.empty_like(self.observed[:F])
+            idx = torch.as_tensor(local, device=self.device)
+            torch.index_select(self.observed, 0, idx, out=self.obs_stage)
+            obs = self.obs_stage
+        key = tuple(int(k) for k in local)
+        if self.use_graph and self._graph is not None \
+                and self._graph_frames == key:
+            self._graph.replay()
+            return
+        self.t_dev.copy_(torch.as_tensor(self.frame_times_all[local],
+                                         dtype=torch.float64))
+        if self.use_graph and contiguous:
+            # warm once eagerly (lazy init inside torch / the driver), then
+            # capture the fixed launch sequence and replay it from now on
+            self._launch_compute(obs)
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self._launch_compute(obs)
+            torch.cuda.current_stream().wait_stream(s)
+            self._graph, self._graph_frames = g, key
+            self._graph.replay()
+        else:
+            self._graph = None      # t_dev / obs changed under the graph
+            self._launch_compute(obs)
+
+    def allreduce(self) -> None:
+        if self.world > 1:
+            torch.distributed.all_reduce(self.Gf, group=self.group)
+            torch.distributed.all_reduce(self.loss_total, group=self.group)
+            cflag = self.coinc.clone()
+            torch.distributed.all_reduce(cflag, op=torch.distributed.ReduceOp.MIN,
+                                         group=self.group)
+            self.coinc.copy_(cflag)
+
+    def check_and_status(self):
+        """Finite guard + the single host sync of the iteration."""
+        lib = _lib.load_library()
+        self.flags.zero_()
+        off = _lib.i64_array(self.layout.offsets)
+        _lib.check(lib.pc_check_finite(
+            _lib.ptr(self.Gf), len(self.layout.segments), off,
+            _lib.ptr(self.flags), _lib.stream()), "pc_check_finite")
+        status = torch.cat([self.loss_total, self.flags.double(),
+                            self.coinc.double()]).cpu().numpy()
+        loss = float(status[0])
+        flags = status[1:1 + len(self.layout.segments)].astype(bool)
+        # pair indices b*M+m stay far below 2**53; INT64_MAX means "none"
+        coinc = int(status[-1]) if status[-1] < 9.0e18 else _lib.INT64_MAX
+        return loss, flags, coinc
+
+    def apply_update(self, lrs: dict, only=None) -> None:
+        """pc_adam_segments (or sgd) for all (or `only`) segments + floors."""
+        lib = _lib.load_library()
+        cfg = self.cfg
+        floors = {"p0": cfg.p0_floor, "a0": cfg.a0_floor,
+                  "sigma": cfg.sigma_floor}
+        segs = [s for s in self.layout.segments
+                if only is None or s.name in only]
+        if not segs:
+            return
+        for s in segs:
+            self.step_count[s.name] += 1
+        # contiguous runs of the flat buffer: pass explicit offsets
+        off, lr, step, fl = [], [], [], []
+        for s in segs:
+            off.append(s.offset)
+            lr.append(lrs[s.group])
+            step.append(self.step_count[s.name])
+            fl.append(floors.get(s.name, -math.inf))
+        off.append(segs[-1].offset + segs[-1].size)
+        if any(segs[i].offset + segs[i].size != segs[i + 1].offset
+               for i in range(len(segs) - 1)):
+            for s in segs:   # non-contiguous subset: one launch per segment
+                self._update_one(s, lrs, floors)
+            return
+        if cfg.optimizer == "adam":
+            _lib.check(lib.pc_adam_segments(
+                _lib.ptr(self.P), _lib.ptr(self.Gf), _lib.ptr(self.Mo),
+                _lib.ptr(self.Vo), len(segs), _lib.i64_array(off),
+                _lib.f64_array(lr), _lib.i32_array(step),
+                _lib.f64_array(fl), _lib.stream()), "pc_adam_segments")
+        else:
+            _lib.check(lib.pc_sgd_segments(
+                _lib.ptr(self.P), _lib.ptr(self.Gf), len(segs),
+                _lib.i64_array(off), _lib.f64_array(lr),
+                _lib.f64_array(fl), _lib.stream()), "pc_sgd_segments")
+
+    def _update_one(self, s, lrs, floors):
+        lib = _lib.load_library()
+        off = _lib.i64_array([s.offset, s.offset + s.size])
+        if self.cfg.optimizer == "adam":
+            _lib.check(lib.pc_adam_segments(
+                _lib.ptr(self.P), _lib.ptr(self.Gf), _lib.ptr(self.Mo),
+                _lib.ptr(self.Vo), 1, off, _lib.f64_array([lrs[s.group]]),
+                _lib.i32_array([self.step_count[s.name]]),
+                _lib.f64_array([floors.get(s.name, -math.inf)]),
+                _lib.stream()), "pc_adam_segments")
+        else:
+            _lib.check(lib.pc_sgd_segments(
+                _lib.ptr(self.P), _lib.ptr(self.Gf), 1, off,
+                _lib.f64_array([lrs[s.group]]),
+                _lib.f64_array([floors.get(s.name, -math.inf)]),
+                _lib.stream()), "pc_sgd_segments")
+
+    def iterate(self, iteration: int, frames: np.ndarray) -> float:
+        """One full iteration; returns the (all-reduced) loss."""
+        cfg = self.cfg
+        lrs = {"coords": scheduled_lr(cfg.lr_coords, iteration,
+                                      cfg.step_size, cfg.drop_rate),
+               "pressure": scheduled_lr(cfg.lr_pressure, iteration,
+                                        cfg.step_size, cfg.drop_rate),
+               "std": scheduled_lr(cfg.lr_std, iteration, cfg.step_size,
+                                   cfg.drop_rate),
+               "deform": scheduled_lr(cfg.lr_deform, iteration,
+                                      cfg.step_size, cfg.drop_rate)}
+        self.last_lrs = lrs
+        self.compute_grads(frames)
+        self.allreduce()
+        loss, flags, coinc = self.check_and_status()
+        if coinc != _lib.INT64_MAX:
+            raise_if_coincident(coinc, self.mu_t, self.darr.positions)
+        if not math.isfinite(loss):
+            raise RuntimeError(f"non-finite loss at iteration {iteration}")
+        if flags.any():
+            # reference order: groups before the first bad one are updated
+            bad_groups = {self.layout.segments[i].group
+                          for i in np.nonzero(flags)[0]}
+            done = []
+            for g in GROUP_ORDER:
+                names = [s.name for s in self.layout.segments
+                         if s.group == g]
+                if g in bad_groups:
+                    self.apply_update(lrs, only=done)
+                    raise ValueError(
+                        f"non-finite gradient in parameter group '{g}'")
+                done += names
+        self.apply_update(lrs)
+        return loss
+
+    # ------------------------------------------------------------ views
+    def cloud(self) -> DynamicCloud:
+        p = {k: v.cpu().numpy().copy() for k, v in self.params.items()}
+        return DynamicCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
+                            p.get("sigma"), p["omega"], basis=self.basis)
+
+    def grads_numpy(self) -> dict:
+        return {k: v.double().cpu().numpy() for k, v in self.grads.items()}
+
+
+def identity_cloud(p0, a0, mu, n_basis: int, basis: str = "gauss"):
+    """Attach identity deformation (reconstruction.py:274-281)."""
+    p0 = np.asarray(p0, dtype=np.float64)
+    B = len(p0)
+    if basis == "polyfourier":
+        return DynamicCloud(p0, a0, mu, None, None, np.zeros((B, 5, n_basis)),
+                            basis="polyfourier")
+    th, sg = default_basis_grid(n_basis)
+    return DynamicCloud(p0, a0, mu, np.broadcast_to(th, (B, n_basis)).copy(),
+                        np.broadcast_to(sg, (B, n_basis)).copy(),
+                        np.zeros((B, 5, n_basis)))

@@ -1,0 +1,268 @@
+"""Drop-in radiator: forward model and adjoint on the B200.
+
+Mirrors pkg/src/pacloud/radiator.py -- ``forward_frame`` (:195-216),
+``frame_state_grads`` (:219-242), ``accumulate_frame_grads`` (:266-294) and
+``CloudGrads`` (:245-263) -- with the same signatures, return shapes and
+exceptions.  NumPy inputs return float64 NumPy outputs (host copies in and
+out); torch CUDA inputs stay on the device.  All arithmetic runs in
+libpacloud_b200.so (pc_forward_traces / pc_residual_state_grads /
+pc_assemble_grads); there is no CPU path.
+
+``DeviceArray`` and the ``*_device`` functions are the zero-copy, batched-
+over-frames layer the fused engine uses.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import BallStateAtT, CloudGrads, CloudState
+
+DEFAULT_SUPPORT_SIGMAS = 6.0
+
+
+def _device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(x, dtype) -> torch.Tensor:
+    """Contiguous CUDA tensor of `dtype` (copies NumPy / host inputs)."""
+    if isinstance(x, torch.Tensor):
+        dev = x.device if x.is_cuda else _device()
+        return x.to(device=dev, dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype,
+                           device=_device()).contiguous()
+
+
+def _is_torch(*xs) -> bool:
+    return any(isinstance(x, torch.Tensor) for x in xs)
+
+
+class DeviceArray:
+    """A SensorArray resident on the device plus its pc_array_t."""
+
+    def __init__(self, array, support_sigmas=DEFAULT_SUPPORT_SIGMAS,
+                 exact=False, positions=None):
+        _lib.load_library()
+        self.array = array
+        self.positions = to_device(
+            array.positions if positions is None else positions,
+            torch.float64)
+        self.M = int(self.positions.shape[0])
+        self.T = int(array.n_samples)
+        self.v = float(array.sound_speed)
+        self.t0 = float(array.t_start)
+        self.dt = 1.0 / float(array.sample_rate)
+        self.support = float(support_sigmas)
+        self.exact = bool(exact)
+        self.struct = _lib.PcArray(
+            self.positions.data_ptr(), self.M, self.T, self.v, self.t0,
+            self.dt, self.support, int(self.exact), 0)
+
+    def plan(self, n_balls: int, n_frames: int) -> dict:
+        """pc_forward_plan: time segment, segments, ball chunks, launches."""
+        lib = _lib.load_library(require_cuda=False)
+        out = (ctypes.c_int32 * 4)()
+        _lib.check(lib.pc_forward_plan(int(n_balls), int(n_frames),
+                                       ctypes.byref(self.struct), out),
+                   "pc_forward_plan")
+        return {"tseg": out[0], "nseg": out[1], "nchunk": out[2],
+                "launches": out[3]}
+
+    def workspace_bytes(self, n_balls: int, n_frames: int) -> int:
+        lib = _lib.load_library()
+        return int(lib.pc_forward_workspace_bytes(
+            int(n_balls), int(n_frames), ctypes.byref(self.struct)))
+
+
+def forward_device(darr: DeviceArray, mu_t, a0_t, p0_t, observed=None,
+                   out=None, loss=None, coincident=None, workspace=None):
+    """pc_forward_traces on device tensors.
+
+    mu_t (F,B,3) f64, a0_t/p0_t (F,B) f32, observed (F,M,T) f32 or None.
+    Returns (out, loss, coincident): out (F,M,T) f32 = predicted traces, or
+    the residual predicted - observed when `observed` is given; loss (F,)
+    f64 per frame (only with observed).
+    """
+    lib = _lib.load_library()
+    F, B = int(a0_t.shape[0]), int(a0_t.shape[1])
+    dev = a0_t.device
+    if out is None:
+        out = torch.empty((F, darr.M, darr.T), dtype=torch.float32,
+                          device=dev)
+    if observed is not None and loss is None:
+        loss = torch.empty(F, dtype=torch.float64, device=dev)
+    if coincident is None:
+        coincident = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64,
+                                device=dev)
+    need = darr.workspace_bytes(max(B, 1), F)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    _lib.check(lib.pc_forward_traces(
+        _lib.ptr(mu_t), _lib.ptr(a0_t), _lib.ptr(p0_t), B, F,
+        ctypes.byref(darr.struct), _lib.ptr(observed), _lib.ptr(out),
+        _lib.ptr(loss) if observed is not None else None,
+        _lib.ptr(coincident), _lib.ptr(workspace), workspace.numel(),
+        _lib.stream()), "pc_forward_traces")
+    return out, loss, coincident
+
+
+def state_grads_device(darr: DeviceArray, mu_t, a0_t, p0_t, residual,
+                       G=None, coincident=None):
+    """pc_residual_state_grads: G (F,B,5) f32 from residual (F,M,T)."""
+    lib = _lib.load_library()
+    F, B = int(a0_t.shape[0]), int(a0_t.shape[1])
+    dev = a0_t.device
+    if G is None:
+        G = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
+    if coincident is None:
+        coincident = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64,
+                                device=dev)
+    _lib.check(lib.pc_residual_state_grads(
+        _lib.ptr(mu_t), _lib.ptr(a0_t), _lib.ptr(p0_t), B, F,
+        ctypes.byref(darr.struct), _lib.ptr(residual), _lib.ptr(G),
+        _lib.ptr(coincident), _lib.stream()), "pc_residual_state_grads")
+    return G, coincident
+
+
+def raise_if_coincident(coincident, mu_t, positions):
+    """radiator.py:186-192: ValueError naming the coincident (ball, sensor)."""
+    c = int(coincident.item()) if isinstance(coincident, torch.Tensor) \
+        else int(coincident)
+    if c == _lib.INT64_MAX:
+        return
+    M = int(positions.shape[0])
+    b, m = divmod(c, M)
+    mu = mu_t.reshape(-1, 3)[b].double().cpu().numpy() \
+        if isinstance(mu_t, torch.Tensor) else np.asarray(mu_t)[b]
+    pos = positions[m].double().cpu().numpy() \
+        if isinstance(positions, torch.Tensor) else np.asarray(positions)[m]
+    d = float(np.linalg.norm(mu - pos))
+    raise ValueError(f"ball {b} coincides with sensor {m} "
+                     f"(distance {d:.3g} mm)")
+
+
+# ---------------------------------------------------------------- drop-ins
+
+def _as_cloud_state(states):
+    """radiator.py:177-183."""
+    if isinstance(states, (list, tuple)):
+        if all(isinstance(s, BallStateAtT) for s in states) or \
+                all(hasattr(s, "a0_t") and np.ndim(s.a0_t) == 0
+                    for s in states):
+            return CloudState.from_states(states)
+        raise TypeError("states must be a CloudState or a list of "
+                        "BallStateAtT")
+    if hasattr(states, "a0_t") and hasattr(states, "mu_t"):
+        return states
+    raise TypeError("states must be a CloudState or a list of BallStateAtT")
+
+
+def _state_tensors(state):
+    mu = to_device(state.mu_t, torch.float64).reshape(1, -1, 3)
+    a0 = to_device(state.a0_t, torch.float32).reshape(1, -1)
+    p0 = to_device(state.p0_t, torch.float32).reshape(1, -1)
+    return mu, a0, p0
+
+
+def _any_nonpositive(x) -> bool:
+    if isinstance(x, torch.Tensor):
+        return bool((x <= 0).any().item())
+    return bool(np.any(np.asarray(x) <= 0))
+
+
+def forward_frame(states, array, support_sigmas: float = DEFAULT_SUPPORT_SIGMAS,
+                  exact: bool = False):
+    """Superpose every ball's pressure trace at every sensor -> (M, T)."""
+    state = _as_cloud_state(states)
+    torch_io = _is_torch(state.a0_t, state.mu_t)
+    darr = DeviceArray(array, support_sigmas, exact)
+    B = len(state)
+    if B == 0:
+        z = torch.zeros((darr.M, darr.T), dtype=torch.float64,
+                        device=_device())
+        return z if torch_io else z.cpu().numpy()
+    if _any_nonpositive(state.a0_t):
+        raise ValueError("all a0_t must be > 0 (clamp before the radiator)")
+    mu, a0, p0 = _state_tensors(state)
+    out, _, coinc = forward_device(darr, mu, a0, p0)
+    raise_if_coincident(coinc, mu, darr.positions)
+    out = out[0].double()
+    return out if torch_io else out.cpu().numpy()
+
+
+def frame_state_grads(states, array, residual,
+                      support_sigmas: float = DEFAULT_SUPPORT_SIGMAS,
+                      exact: bool = False):
+    """Gradient of 0.5*||residual||^2 w.r.t. (a0_t, p0_t, mu_t) -> (B, 5)."""
+    state = _as_cloud_state(states)
+    torch_io = _is_torch(state.a0_t, state.mu_t, residual)
+    M, T = array.positions.shape[0], int(array.n_samples)
+    if tuple(residual.shape) != (M, T):
+        raise ValueError(
+            f"residual shape {tuple(residual.shape)} does not match the "
+            f"array ({M}, {T})")
+    B = len(state)
+    if B == 0:
+        z = torch.zeros((0, 5), dtype=torch.float64, device=_device())
+        return z if torch_io else z.cpu().numpy()
+    darr = DeviceArray(array, support_sigmas, exact)
+    mu, a0, p0 = _state_tensors(state)
+    r = to_device(residual, torch.float32).reshape(1, M, T)
+    G, coinc = state_grads_device(darr, mu, a0, p0, r)
+    raise_if_coincident(coinc, mu, darr.positions)
+    G = G[0].double()
+    return G if torch_io else G.cpu().numpy()
+
+
+def accumulate_frame_grads(states, state_grads, array, residual,
+                           support_sigmas: float = DEFAULT_SUPPORT_SIGMAS,
+                           exact: bool = False) -> CloudGrads:
+    """Compose radiator and deformation partials into parameter gradients."""
+    lib = _lib.load_library()
+    state = _as_cloud_state(states)
+    torch_io = _is_torch(state.a0_t, residual, state_grads.d_omega)
+    M, T = array.positions.shape[0], int(array.n_samples)
+    if tuple(residual.shape) != (M, T):
+        raise ValueError(
+            f"residual shape {tuple(residual.shape)} does not match the "
+            f"array ({M}, {T})")
+    sg = state_grads
+    B, _, N = tuple(sg.d_omega.shape)
+    dev = _device()
+    shared = bool(sg.shared_basis)
+    has_ts = sg.d_theta is not None and np.prod(sg.d_theta.shape) > 0
+    if B == 0:
+        G = torch.zeros((1, 0, 5), dtype=torch.float32, device=dev)
+    else:
+        darr = DeviceArray(array, support_sigmas, exact)
+        mu, a0, p0 = _state_tensors(state)
+        r = to_device(residual, torch.float32).reshape(1, M, T)
+        G, coinc = state_grads_device(darr, mu, a0, p0, r)
+        raise_if_coincident(coinc, mu, darr.positions)
+    d_base = to_device(sg.d_base, torch.float64)
+    d_om = to_device(sg.d_omega, torch.float64)
+    d_th = to_device(sg.d_theta, torch.float64) if has_ts else None
+    d_sg = to_device(sg.d_sigma, torch.float64) if has_ts else None
+    f64 = dict(dtype=torch.float64, device=dev)
+    g_p0 = torch.zeros(B, **f64)
+    g_a0 = torch.zeros(B, **f64)
+    g_mu = torch.zeros((B, 3), **f64)
+    ts_shape = ((B, N) if shared else (B, 5, N)) if has_ts else (B, 0)
+    g_th = torch.zeros(ts_shape, **f64)
+    g_sg = torch.zeros(ts_shape, **f64)
+    g_om = torch.zeros((B, 5, N), **f64)
+    rows = _lib.i32_array(np.asarray(sg.omega_row).ravel()[:5])
+    _lib.check(lib.pc_assemble_grads(
+        _lib.ptr(G), B, N, _lib.ptr(d_base), _lib.ptr(d_om), _lib.ptr(d_th),
+        _lib.ptr(d_sg), rows, int(shared), int(has_ts), _lib.ptr(g_p0),
+        _lib.ptr(g_a0), _lib.ptr(g_mu), _lib.ptr(g_th), _lib.ptr(g_sg),
+        _lib.ptr(g_om), _lib.stream()), "pc_assemble_grads")
+    out = [g_p0, g_a0, g_mu, g_th, g_sg, g_om]
+    if not torch_io:
+        out = [x.cpu().numpy() for x in out]
+    return CloudGrads(*out)

@@ -1,0 +1,424 @@
+"""CUDA path vs the CPU oracle / golden vectors (all calls go through the
+C ABI via the drop-in API).  Tolerances: signals 1e-5 and gradients 1e-4
+relative L2 (BASELINE.json); masks, orders and exactness properties
+bit-exact."""
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import GRAD_TOL, SIGNAL_TOL, planar_array, rel_l2, small_array
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pc():
+    import paper_2412_03898_b200 as pc
+    from paper_2412_03898_b200 import _lib
+    _lib.load_library()
+    return pc
+
+
+def _state(pc, a0, p0, mu):
+    return pc.CloudState(np.asarray(a0, float), np.asarray(p0, float),
+                         np.asarray(mu, float))
+
+
+# ------------------------------------------------------------ forward
+
+def test_forward_small_golden(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    st = _state(pc, golden["small_a0"], golden["small_p0"], golden["small_mu"])
+    assert rel_l2(pc.forward_frame(st, arr), golden["small_fwd"]) < SIGNAL_TOL
+    assert rel_l2(pc.forward_frame(st, arr, exact=True),
+                  golden["small_fwd_exact"]) < SIGNAL_TOL
+
+
+def test_forward_planar_golden(pc, golden):
+    arr = planar_array(golden, pc.SensorArray)
+    st = _state(pc, golden["planar_a0"], golden["planar_p0"],
+                golden["planar_mu"])
+    assert rel_l2(pc.forward_frame(st, arr), golden["planar_pred"]) \
+        < SIGNAL_TOL
+
+
+def test_forward_empty_cloud(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    out = pc.forward_frame(_state(pc, np.zeros(0), np.zeros(0),
+                                  np.zeros((0, 3))), arr)
+    assert out.shape == (8, 64) and np.all(out == 0.0)
+
+
+def test_two_identical_balls_double_exactly(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    one = _state(pc, [0.7], [1.3], [[1.0, -2.0, 0.5]])
+    two = _state(pc, [0.7, 0.7], [1.3, 1.3], [[1.0, -2.0, 0.5]] * 2)
+    assert np.array_equal(pc.forward_frame(two, arr),
+                          2.0 * pc.forward_frame(one, arr))
+
+
+def test_p0_scaling_exact(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    s1 = _state(pc, [0.7], [0.6], [[1.0, -2.0, 0.5]])
+    s2 = _state(pc, [0.7], [1.2], [[1.0, -2.0, 0.5]])
+    assert np.array_equal(pc.forward_frame(s2, arr),
+                          2.0 * pc.forward_frame(s1, arr))
+
+
+def test_coincident_ball_and_sensor(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    st = _state(pc, [0.5], [1.0], [arr.positions[3]])
+    with pytest.raises(ValueError, match=r"ball 0 .* sensor 3"):
+        pc.forward_frame(st, arr)
+    with pytest.raises(ValueError, match=r"ball 0 .* sensor 3"):
+        pc.frame_state_grads(st, arr, np.ones((8, 64)))
+
+
+def test_nonpositive_a0_rejected(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    with pytest.raises(ValueError, match="a0_t must be > 0"):
+        pc.forward_frame(_state(pc, [0.0], [1.0], [[1, 2, 3]]), arr)
+
+
+def test_fast_path_matches_exact(pc, golden, rng):
+    arr = small_array(golden, pc.SensorArray)
+    st = _state(pc, rng.uniform(0.3, 1, 5), rng.uniform(0.2, 1, 5),
+                rng.uniform(-4, 4, (5, 3)))
+    fast = pc.forward_frame(st, arr)
+    exact = pc.forward_frame(st, arr, exact=True)
+    assert np.max(np.abs(fast - exact)) < 1e-6 * np.max(np.abs(exact))
+
+
+def test_near_field_ball_close_to_sensor(pc):
+    """R < 10 a0: the (R + v t) term matters (t = 0 profile)."""
+    arr = pc.SensorArray(np.array([[2.0, 0.0, 0.0], [0.0, 30.0, 0.0]]), 1.5,
+                         20.0, 400, 0.0)
+    st = _state(pc, [0.8, 0.5], [1.0, 0.7], [[0.0, 0.0, 0.0],
+                                             [0.3, 0.2, -0.1]])
+    for exact in (False, True):
+        got = pc.forward_frame(st, arr, exact=exact)
+        ref = oracle.forward_frame(st, arr, exact=exact)
+        assert rel_l2(got, ref) < SIGNAL_TOL
+        G = pc.frame_state_grads(st, arr, ref * 0.3, exact=exact)
+        Gr = oracle.frame_state_grads(st, arr, ref * 0.3, exact=exact)
+        assert rel_l2(G, Gr) < GRAD_TOL
+
+
+# ------------------------------------------------------------ adjoint
+
+def test_adjoint_small_golden(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    st = _state(pc, golden["small_a0"], golden["small_p0"], golden["small_mu"])
+    G = pc.frame_state_grads(st, arr, golden["small_res"])
+    assert rel_l2(G, golden["small_G"]) < GRAD_TOL
+    G = pc.frame_state_grads(st, arr, golden["small_res"], exact=True)
+    assert rel_l2(G, golden["small_G_exact"]) < GRAD_TOL
+
+
+def test_adjoint_planar_golden(pc, golden):
+    arr = planar_array(golden, pc.SensorArray)
+    st = _state(pc, golden["planar_a0"], golden["planar_p0"],
+                golden["planar_mu"])
+    G = pc.frame_state_grads(st, arr, golden["planar_res"])
+    assert rel_l2(G, golden["planar_G"]) < GRAD_TOL
+    for col in range(5):   # every state column, not just the dominant ones
+        assert rel_l2(G[:, col], golden["planar_G"][:, col]) < GRAD_TOL
+
+
+def test_zero_residual_zero_gradient(pc, golden, rng):
+    arr = small_array(golden, pc.SensorArray)
+    st = _state(pc, rng.uniform(0.3, 1, 3), rng.uniform(0.2, 1, 3),
+                rng.uniform(-4, 4, (3, 3)))
+    assert np.all(pc.frame_state_grads(st, arr, np.zeros((8, 64))) == 0.0)
+
+
+def test_residual_shape_rejected(pc, golden):
+    arr = small_array(golden, pc.SensorArray)
+    st = _state(pc, [0.5], [1.0], [[0, 0, 0]])
+    with pytest.raises(ValueError, match="does not match"):
+        pc.frame_state_grads(st, arr, np.zeros((8, 63)))
+
+
+# ------------------------------------------------------------ deformation
+
+@pytest.mark.parametrize("tag", ["sh", "pc"])
+@pytest.mark.parametrize("mode", ["multiplicative", "additive", "radial"])
+def test_deformation_golden(pc, golden, tag, mode):
+    g = golden
+    ks = ("p0", "a0", "mu", "theta", "sigma", "omega")
+    cloud = pc.DynamicCloud(*[g[f"def_{tag}_{k}"] for k in ks])
+    key = f"def_{tag}_{mode[:3]}"
+    st = pc.cloud_states_at(cloud, 0.37, mode, a0_floor=0.3)
+    assert rel_l2(st.a0_t, g[key + "_a0t"]) < 1e-7
+    assert rel_l2(st.p0_t, g[key + "_p0t"]) < 1e-7
+    assert rel_l2(st.mu_t, g[key + "_mut"]) < 1e-13
+    jac = pc.cloud_state_grads(cloud, 0.37, mode, a0_floor=0.3)
+    for nm, arr in (("dbase", jac.d_base), ("domega", jac.d_omega),
+                    ("dtheta", jac.d_theta), ("dsigma", jac.d_sigma)):
+        assert rel_l2(arr, g[key + "_" + nm]) < 1e-12, nm
+    arr_ = small_array(golden, pc.SensorArray)
+    # radiator input: the golden fp64 states, so only the chain rule + adjoint
+    # are under test here
+    gst = _state(pc, g[key + "_a0t"], g[key + "_p0t"], g[key + "_mut"])
+    cg = pc.accumulate_frame_grads(gst, jac, arr_, g[key + "_res"])
+    for nm in ("p0", "a0", "mu", "theta", "sigma", "omega"):
+        assert rel_l2(getattr(cg, nm), g[key + "_g" + nm]) < GRAD_TOL, nm
+
+
+def test_identity_deformation_bit_exact(pc, rng):
+    B, nb = 6, 65
+    a0 = rng.uniform(0.1, 1, B).astype(np.float32).astype(float)
+    p0 = rng.uniform(0.1, 2, B).astype(np.float32).astype(float)
+    mu = rng.uniform(-5, 5, (B, 3))
+    cloud = pc.DynamicCloud.static(p0, a0, mu, n_basis=nb)
+    for t in np.linspace(0, 1, 5):
+        st = pc.cloud_states_at(cloud, float(t))
+        assert np.array_equal(st.a0_t, a0)
+        assert np.array_equal(st.p0_t, p0)
+        assert np.array_equal(st.mu_t, mu)
+
+
+def test_clamped_a0_zero_gradient(pc):
+    omega = np.zeros((1, 5, 2))
+    omega[0, 0, :] = -0.8
+    cloud = pc.DynamicCloud(np.array([1.0]), np.array([0.5]), np.zeros((1, 3)),
+                            np.array([[0.4, 0.6]]), np.array([[0.3, 0.3]]),
+                            omega)
+    cg = pc.cloud_state_grads(cloud, 0.5, a0_floor=1.0)
+    assert cg.d_base[0, 0] == 0.0 and np.all(cg.d_omega[0, 0] == 0.0)
+    assert pc.cloud_states_at(cloud, 0.5, a0_floor=1.0).a0_t[0] == 1.0
+
+
+# ------------------------------------------------------------ loss / Adam
+
+def test_l2_loss(pc, rng):
+    p = rng.normal(size=(5, 9))
+    o = rng.normal(size=(5, 9))
+    assert pc.l2_loss(p, o) == pytest.approx(oracle.l2_loss(p, o), rel=1e-12)
+    assert pc.l2_loss(np.ones((2, 4)), np.zeros((2, 4))) == 4.0
+    with pytest.raises(ValueError):
+        pc.l2_loss(np.zeros((2, 3)), np.zeros((3, 2)))
+
+
+def test_adam_golden(pc, golden):
+    p = golden["adam_p0"].copy()
+    st = pc.AdamState.like(p)
+    for k in range(3):
+        pc.adam_step(p, golden["adam_g"][k], st, lr=1e-2 * (k + 1))
+        # gradients travel as float32: parameters agree to ~1e-9 relative
+        assert rel_l2(p, golden["adam_traj"][k]) < 1e-8
+    assert st.t == 3
+
+
+def test_adam_known_answers(pc):
+    p = np.array([3.0])
+    st = pc.AdamState.like(p)
+    pc.adam_step(p, np.array([1.0]), st, lr=0.1)
+    assert p[0] == pytest.approx(2.9, abs=1e-6)
+    p = np.array([1.5, -2.0])
+    st = pc.AdamState.like(p)
+    pc.adam_step(p, np.zeros(2), st, lr=0.1)
+    assert np.array_equal(p, [1.5, -2.0])
+    with pytest.raises(ValueError, match="pressure"):
+        pc.adam_step(p, np.array([np.nan, 0.0]), st, 0.1, "pressure")
+    assert np.array_equal(p, [1.5, -2.0])   # raised before mutation
+
+
+def test_prune_golden(pc, golden):
+    import torch
+    from paper_2412_03898_b200 import _lib
+    lib = _lib.load_library()
+    p0 = torch.as_tensor(golden["prune_p0"], device="cuda")
+    keep = torch.empty(len(p0), dtype=torch.uint8, device="cuda")
+    nk = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.pc_prune_mask(p0.data_ptr(), len(p0), 1e-2,
+                                 keep.data_ptr(), nk.data_ptr(), ws.data_ptr(),
+                                 ws.numel(), _lib.stream()), "prune")
+    assert np.array_equal(keep.cpu().numpy(), golden["prune_keep"])
+    assert int(nk.item()) == int(golden["prune_keep"].sum())
+    from paper_2412_03898_b200.reconstruction import keep_index
+    idx = keep_index(keep)
+    assert np.array_equal(idx.cpu().numpy(), golden["prune_order"])
+
+
+@pytest.mark.parametrize("B", [1, 1000, 1024, 5000, 70001])
+def test_compaction_bit_exact(pc, B):
+    import torch
+    from paper_2412_03898_b200 import _lib
+    from paper_2412_03898_b200.reconstruction import gather_rows
+    lib = _lib.load_library()
+    rng = np.random.default_rng(B)
+    keep = rng.uniform(size=B) < 0.7
+    app = (rng.uniform(size=B) < 0.1) & keep
+    k = torch.as_tensor(keep.astype(np.uint8), device="cuda")
+    a = torch.as_tensor(app.astype(np.uint8), device="cuda")
+    ws = torch.empty(lib.pc_compact_workspace_bytes(B), dtype=torch.uint8,
+                     device="cuda")
+    idx = torch.empty(2 * B, dtype=torch.int64, device="cuda")
+    n = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(lib.pc_compact_index(k.data_ptr(), a.data_ptr(), B,
+                                    idx.data_ptr(), n.data_ptr(),
+                                    ws.data_ptr(), ws.numel(), _lib.stream()),
+               "compact")
+    _, _, want, _ = oracle.densify_plan(np.where(keep, 1.0, 0.0),
+                                        np.where(app, 1.0, 0.0), p0_min=0.5,
+                                        q=100.0)
+    want = np.concatenate([np.nonzero(keep)[0], np.nonzero(app)[0]])
+    got = idx[:int(n.item())].cpu().numpy()
+    assert np.array_equal(got, want)
+    rows = rng.normal(size=(B, 7))
+    g = gather_rows(rows, idx[:int(n.item())])
+    assert np.array_equal(g, rows[want])
+
+
+# ------------------------------------------------------------ end to end
+
+def test_dynamic_reconstruct_golden(pc, golden):
+    """Three reference iterations through the fused engine."""
+    g = golden
+    arr = small_array(golden, pc.SensorArray)
+    obs = pc.SignalSet(g["dyn_data"], pc.frame_times(3))
+    init = [type("Ball", (), dict(p0=g["dyn_p0"][i], a0=g["dyn_a0"][i],
+                                  mu=g["dyn_mu"][i]))() for i in range(4)]
+    cfg = pc.ReconConfig(lr_coords=5e-3, lr_pressure=2e-2, lr_std=2e-3,
+                         lr_deform=5e-3, dynamic_iters=3, n_basis=9, seed=2)
+    log = []
+    cloud = pc.dynamic_reconstruct(obs, arr, init, cfg, progress=log.append)
+    losses = [r["loss"] for r in log]
+    assert rel_l2(losses, g["dyn_loss"]) < SIGNAL_TOL
+    for nm in ("p0", "a0", "mu", "theta", "sigma", "omega"):
+        ref = g["dyn_out_" + nm]
+        got = getattr(cloud, nm)
+        if nm == "omega":
+            # after three sign-like Adam steps omega ~ +-lr: compare updates
+            assert rel_l2(got, ref) < 1e-3, nm
+        else:
+            assert rel_l2(got, ref) < 1e-6, nm
+
+
+@pytest.mark.parametrize("mode", ["multiplicative", "additive", "radial"])
+def test_end_to_end_fd(pc, rng, mode):
+    """reference test_radiator.py:187-226: assembled gradient vs central
+    differences of the oracle loss (CUDA gradient, exact=True)."""
+    from pacloud_fd import end_to_end_problem
+    arr, observed, x0, unpack, total_loss = end_to_end_problem(pc, rng, mode)
+    cloud = unpack(x0)
+    st = pc.cloud_states_at(cloud, 0.55, mode)
+    sg = pc.cloud_state_grads(cloud, 0.55, mode)
+    resid = oracle.forward_frame(oracle.cloud_states_at(cloud, 0.55, mode),
+                                 arr, exact=True) - observed
+    g = pc.accumulate_frame_grads(st, sg, arr, resid, exact=True)
+    ana = np.concatenate([g.p0, g.a0, g.mu.ravel(), g.theta.ravel(),
+                          g.sigma.ravel(), g.omega.ravel()])
+    from helpers import fd_gradient, rel_err
+    num = fd_gradient(total_loss, x0, 1e-5)
+    assert np.max(rel_err(ana, num, floor_rel=1e-5)) < 1e-4
+
+
+def _engine_vs_oracle(pc, prob, obs, frames=None, tol_g=GRAD_TOL):
+    from paper_2412_03898_b200.engine import IterationEngine
+    cfg = prob.config
+    eng = IterationEngine(prob.cloud, prob.array, obs, prob.frame_times, cfg)
+    frames = np.arange(prob.n_frames) if frames is None else frames
+    eng.compute_grads(frames)
+    loss, flags, coinc = eng.check_and_status()
+    g = eng.grads_numpy()
+    ref_loss, ref = oracle.iteration_grads(
+        prob.cloud, prob.frame_times[frames], obs[frames].astype(np.float64),
+        prob.array, cfg, basis=prob.cloud.basis)
+    assert not flags.any()
+    assert abs(loss - ref_loss) / ref_loss < SIGNAL_TOL
+    keys = ("p0", "a0", "mu", "omega") if prob.cloud.basis != "gauss" else \
+        ("p0", "a0", "mu", "theta", "sigma", "omega")
+    for k in keys:
+        assert rel_l2(g[k], getattr(ref, k)) < tol_g, k
+    return eng
+
+
+def _observed(prob, threads=0):
+    return np.stack([oracle.forward_frame(oracle.States(a, p, m), prob.array,
+                                          threads=threads)
+                     for a, p, m in prob.gt_frames]).astype(np.float32)
+
+
+def test_engine_config2_reduced(pc):
+    from paper_2412_03898_b200 import synth
+    prob = synth.make_problem(2, n_balls=1500, n_sensors=128, n_frames=3)
+    obs = _observed(prob)
+    eng = _engine_vs_oracle(pc, prob, obs)
+    # graph replay reproduces the eager result bit-exactly
+    g1 = eng.Gf.clone()
+    eng.compute_grads(np.arange(prob.n_frames))
+    assert bool((eng.Gf == g1).all())
+
+
+def test_engine_gauss_basis_per_channel(pc):
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.core import DynamicCloud, ReconConfig
+    prob = synth.make_problem(2, n_balls=400, n_sensors=64, n_frames=4)
+    rng = np.random.default_rng(5)
+    B, nb = 400, 9
+    c = prob.cloud
+    theta = np.tile(np.linspace(0, 1, nb), (B, 5, 1)) + \
+        rng.uniform(-0.02, 0.02, (B, 5, nb))
+    sigma = np.full((B, 5, nb), 0.25)
+    omega = rng.uniform(-0.02, 0.02, (B, 5, nb))
+    prob.cloud = DynamicCloud(c.p0, c.a0, c.mu, theta, sigma, omega)
+    prob.config = ReconConfig(n_basis=nb, coord_mode="radial")
+    _engine_vs_oracle(pc, prob, _observed(prob))
+
+
+def test_engine_config1_full(pc):
+    """BASELINE config 1 at full size (4096 balls x 256 sensors x 2048)."""
+    from paper_2412_03898_b200 import synth
+    prob = synth.make_problem(1)
+    obs = _observed(prob)
+    eng = _engine_vs_oracle(pc, prob, obs)
+    # forward signal parity at full size
+    st = oracle.States(prob.cloud.a0, prob.cloud.p0, prob.cloud.mu)
+    pred_ref = oracle.forward_frame(st, prob.array)
+    got = eng.resid[0].double().cpu().numpy() + obs[0]
+    assert rel_l2(got, pred_ref) < SIGNAL_TOL
+
+
+def test_engine_minibatch_frames_and_steps(pc):
+    """frame_batch minibatch + Adam steps vs the oracle loop."""
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.engine import IterationEngine, select_frames
+    prob = synth.make_problem(5, n_balls=600, n_sensors=48, n_frames=6)
+    obs = _observed(prob)
+    cfg = prob.config
+    eng = IterationEngine(prob.cloud, prob.array, obs, prob.frame_times, cfg)
+    rng_a = np.random.default_rng(3)
+    rng_b = np.random.default_rng(3)
+    cl = prob.cloud
+    ref_cloud = type("C", (), {})()
+    for k in ("p0", "a0", "mu", "omega"):
+        setattr(ref_cloud, k, getattr(cl, k).copy())
+    ref_cloud.theta = cl.theta
+    ref_cloud.sigma = cl.sigma
+    moments = {k: oracle.Moments(np.zeros_like(getattr(ref_cloud, k)),
+                                 np.zeros_like(getattr(ref_cloud, k)))
+               for k in ("p0", "a0", "mu", "omega")}
+    for it in range(3):
+        fr_a = select_frames(prob.n_frames, 3, rng_a)
+        fr_b = select_frames(prob.n_frames, 3, rng_b)
+        assert np.array_equal(fr_a, fr_b)
+        loss = eng.iterate(it, fr_a)
+        ref_loss, grads = oracle.iteration_grads(
+            ref_cloud, prob.frame_times[fr_b], obs[fr_b].astype(np.float64),
+            prob.array, cfg, basis="polyfourier")
+        assert abs(loss - ref_loss) / ref_loss < SIGNAL_TOL
+        lrs = {"pressure": cfg.lr_pressure, "std": cfg.lr_std,
+               "coords": cfg.lr_coords, "deform": cfg.lr_deform}
+        oracle.apply_step(ref_cloud, grads, moments, lrs, cfg,
+                          basis="polyfourier")
+    got = eng.cloud()
+    for k in ("p0", "a0", "mu", "omega"):
+        init = getattr(cl, k)
+        assert rel_l2(getattr(got, k), getattr(ref_cloud, k)) < 1e-8, k
+        # the Adam updates themselves (sign-like steps) agree closely
+        assert rel_l2(getattr(got, k) - init,
+                      getattr(ref_cloud, k) - init) < 1e-2, k
