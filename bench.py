@@ -229,7 +229,8 @@ def workload_config(cfg_id, prob, world):
 def run_ours(args, rank, world, local):
     import torch
     from paper_2412_03898_b200 import _lib, synth
-    from paper_2412_03898_b200.engine import IterationEngine, shard_range
+    from paper_2412_03898_b200.distributed import frame_shard, shard_range
+    from paper_2412_03898_b200.engine import IterationEngine
     from paper_2412_03898_b200.radiator import DeviceArray, forward_device
 
     torch.cuda.set_device(local)
@@ -261,13 +262,12 @@ def run_ours(args, rank, world, local):
     if sensor_shard:
         lo, hi = shard_range(M, rank, world)
         eng = IterationEngine(prob.cloud, arr, obs[:, lo:hi].contiguous(),
-                              prob.frame_times, cfg, sensors=(lo, hi))
+                              prob.frame_times, cfg, shard="sensors")
         local_frames = frames_all
     else:
-        lo, hi = shard_range(F, rank, world)
-        local_frames = frames_all[lo:hi]
+        local_frames = frame_shard(frames_all, rank, world)
         eng = IterationEngine(prob.cloud, arr, obs, prob.frame_times, cfg,
-                              frames=local_frames if world > 1 else None)
+                              shard="frames")
     del obs
     torch.cuda.synchronize()
 
@@ -309,7 +309,6 @@ def run_ours(args, rank, world, local):
     # ---- dominant kernels: fwd + adj, timed live with events on the
     # launching stream (eager, same buffers), and exact algorithmic work
     F_loc = len(local_frames)
-    idx = np.arange(F_loc) if not sensor_shard else frames_all
     eng.t_dev.copy_(torch.as_tensor(prob.frame_times[local_frames]))
     from paper_2412_03898_b200.deformation import deform_states_device
     from paper_2412_03898_b200.radiator import state_grads_device

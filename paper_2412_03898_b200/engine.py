@@ -19,10 +19,10 @@ Parameters live in one flat float64 buffer (group order pressure, std,
 coords, deform -- the reference's update order), gradients in a float32
 buffer with the same offsets, Adam moments in float64.
 
-Sharding: ``frames`` restricts a rank to a subset of the
-selected frames (frame sharding); ``sensors=(lo, hi)`` restricts it to a
-sensor slice for every frame (sensor sharding; ball states are recomputed
-on every rank, i.e. broadcast).  Both end in the same gradient all-reduce.
+Sharding (distributed.py): ``shard="frames"`` gives each rank
+a contiguous block of every iteration's selected frames; ``shard="sensors"``
+gives it a sensor block for every frame (ball states recomputed on every
+rank, i.e. broadcast).  Both end in the same gradient all-reduce.
 """
 
 from __future__ import annotations
@@ -37,6 +37,7 @@ from . import _lib
 from .core import DynamicCloud, default_basis_grid
 from .deformation import (DeviceCloud, deform_backward_device,
                           deform_states_device)
+from .distributed import allreduce_iteration, frame_shard, shard_range
 from .radiator import (DeviceArray, forward_device, raise_if_coincident,
                        state_grads_device, to_device)
 
@@ -55,13 +56,6 @@ def select_frames(n_frames: int, batch: int, rng) -> np.ndarray:
     if batch <= 0 or batch >= n_frames:
         return np.arange(n_frames)
     return np.sort(rng.choice(n_frames, size=batch, replace=False))
-
-
-def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous block [lo, hi) of n items owned by `rank` of `world`."""
-    lo = (n * rank) // world
-    hi = (n * (rank + 1)) // world
-    return lo, hi
 
 
 @dataclass
@@ -101,8 +95,8 @@ class IterationEngine:
     """Device-resident parameters, Adam state and per-iteration buffers."""
 
     def __init__(self, cloud, array, observed, frame_times, config, *,
-                 frames=None, sensors=None, process_group=None,
-                 use_graph=True, device=None):
+                 shard=None, process_group=None, use_graph=True,
+                 device=None):
         _lib.load_library()
         self.cfg = config
         self.basis = getattr(cloud, "basis", getattr(config, "basis",
@@ -110,14 +104,17 @@ class IterationEngine:
         self.device = device or torch.device("cuda",
                                              torch.cuda.current_device())
         self.group = process_group
-        self.world = (torch.distributed.get_world_size(process_group)
-                      if process_group is not None
-                      or (torch.distributed.is_available()
-                          and torch.distributed.is_initialized()) else 1)
+        dist = torch.distributed
+        self.world = dist.get_world_size(process_group) if (
+            dist.is_available() and dist.is_initialized()) else 1
+        self.rank = dist.get_rank(process_group) if self.world > 1 else 0
+        if shard not in (None, "frames", "sensors"):
+            raise ValueError("shard must be None, 'frames' or 'sensors'")
+        self.shard = shard if self.world > 1 else None
         self.frame_times_all = np.asarray(frame_times, dtype=np.float64)
         self.n_frames_all = len(self.frame_times_all)
-        self.local_frames = None if frames is None else np.asarray(frames)
-        lo, hi = sensors if sensors is not None else (0, array.n_sensors)
+        lo, hi = (shard_range(array.n_sensors, self.rank, self.world)
+                  if self.shard == "sensors" else (0, array.n_sensors))
         self.sensors = (int(lo), int(hi))
         pos = np.asarray(array.positions)[lo:hi]
         self.darr = DeviceArray(array, config.support_sigmas,
@@ -186,11 +183,9 @@ class IterationEngine:
         self._graph = None
 
     def _local_frames(self, frames: np.ndarray) -> np.ndarray:
-        if self.local_frames is not None:
-            mine = set(int(k) for k in self.local_frames)
-            return np.array([k for k in frames if int(k) in mine],
-                            dtype=np.int64)
-        return frames
+        if self.shard == "frames":
+            return frame_shard(frames, self.rank, self.world)
+        return np.asarray(frames, dtype=np.int64)
 
     # ------------------------------------------------------------ compute
     def _launch_compute(self, obs):
@@ -255,12 +250,8 @@ class IterationEngine:
 
     def allreduce(self) -> None:
         if self.world > 1:
-            torch.distributed.all_reduce(self.Gf, group=self.group)
-            torch.distributed.all_reduce(self.loss_total, group=self.group)
-            cflag = self.coinc.clone()
-            torch.distributed.all_reduce(cflag, op=torch.distributed.ReduceOp.MIN,
-                                         group=self.group)
-            self.coinc.copy_(cflag)
+            allreduce_iteration(self.Gf, self.loss_total, self.coinc,
+                                self.group)
 
     def check_and_status(self):
         """Finite guard + the single host sync of the iteration."""
