@@ -56,6 +56,9 @@ typedef struct pc_array {
     double support_sigmas;   /* radiator.py:31 DEFAULT_SUPPORT_SIGMAS */
     int32_t exact;           /* evaluate every sample (radiator.py:100-102) */
     int32_t reserved;
+    const int32_t *sensor_order; /* device, (M,) processing order of the
+                                    sensors (spatially clustered) or NULL;
+                                    outputs stay in sensor index order */
 } pc_array_t;
 
 /* DynamicCloud (core.py:166-259), device f64 arrays.

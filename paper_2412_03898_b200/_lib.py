@@ -30,7 +30,7 @@ class PcArray(Structure):
                 ("n_samples", c_int32), ("sound_speed", c_double),
                 ("t_start", c_double), ("dt", c_double),
                 ("support_sigmas", c_double), ("exact", c_int32),
-                ("reserved", c_int32)]
+                ("reserved", c_int32), ("sensor_order", c_void_p)]
 
 
 class PcCloud(Structure):

@@ -19,6 +19,35 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): one issue slot
+// and one FMA-pipe slot for two lanes' worth of work.
+__device__ __forceinline__ unsigned long long f2u(float2 a) {
+    return (unsigned long long)__float_as_uint(a.x) |
+           ((unsigned long long)__float_as_uint(a.y) << 32);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long u) {
+    return make_float2(__uint_as_float((unsigned)u), __uint_as_float((unsigned)(u >> 32)));
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 ex2_2(float2 x) { return make_float2(ex2(x.x), ex2(x.y)); }
+// 2^-xx per component (the negation folds into MUFU.EX2's operand)
+__device__ __forceinline__ float2 ex2n_2(float2 xx) { return make_float2(ex2(-xx.x), ex2(-xx.y)); }
+__device__ __forceinline__ float2 splat2(float v) { return make_float2(v, v); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -49,19 +78,16 @@ inline int num_sms() {
 
 inline cudaStream_t as_stream(pc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Per-(ball, sensor) window and fp64 offsets, shared by forward and adjoint.
-// Follows radiator.py:93-112 with the reciprocals of v and dt hoisted (the
-// window edge can move by one sample only where (R +- 6a)/v lands exactly on
-// a sample time; those samples weigh exp(-18) of the peak).
-struct PairGeom {
-    double R;
-    int jlo, jhi;  // clipped to [0, T)
-    int jc;        // reference sample for the fp32 offsets (near the peak)
-    float Dc;      // R - v*t(jc), fp32 of an fp64 difference
-    float Uc;      // R + v*t(jc)
-    bool near;     // the (R + v t) term matters somewhere in the window
-};
-
+// Per-(ball, sensor) window and fp64 wavefront offsets, shared by forward
+// and adjoint.  Follows radiator.py:93-112 with the reciprocals of v and dt
+// hoisted (an edge sample can move only where (R +- 6a)/v lands exactly on a
+// sample time; such samples weigh exp(-18) of the peak).
+//
+// Samples are evaluated in scaled units x = s * (R - v t), s = sqrt(log2 e /
+// 2) / a0, so exp(-(R - v t)^2 / (2 a0^2)) = 2^(-x^2) is one FMUL + MUFU.EX2.
+// X (and Y for the near-field R + v t term) are x at the window start, formed
+// in fp64 and rounded once; per sample x = X - k * (s v dt) in fp32 with an
+// exact integer k, so the error stays ~1e-7 of a0.
 struct ArrayConsts {
     double v, t0, dt, inv_v, inv_dt, support;
     float vdt;
@@ -69,32 +95,67 @@ struct ArrayConsts {
     int exact;
 };
 
-__device__ __forceinline__ void pair_geometry(double dx, double dy, double dz, float a0,
-                                              const ArrayConsts& ac, PairGeom& g) {
-    g.R = sqrt(dx * dx + dy * dy + dz * dz);
-    const double R = g.R;
+constexpr float kHalfLog2e = 0.72134752044448170f;   // log2(e) / 2
+constexpr float kKappa = 1.3862943611198906f;        // 2 / log2(e) = 1/(s a)^2
+
+__device__ __forceinline__ float scale_of(float a0) { return sqrtf(kHalfLog2e) / a0; }
+
+struct PairSetup {
+    double R;
+    int jl, jh;    // window clipped to [clip_lo, clip_hi)
+    int jr;        // reference sample: nearest the (R - v t) wavefront, in window
+    float X, Y;    // s (R -/+ v t_jr)
+    bool near;     // the (R + v t) term exceeds exp(-50) of the peak somewhere
+};
+
+// Window and offsets of one pair.  R is refined from an fp32 estimate by one
+// fp64 Newton step (|error| ~ 1e-16 R); the window bounds and the reference
+// sample come from the fp32 wavefront position (an edge can move by one
+// sample only within ~1e-3 sample of a boundary, where the Gaussian weighs
+// exp(-18)); the wavefront offsets X, Y are differences formed in fp64.
+__device__ __forceinline__ void pair_setup(double dx, double dy, double dz, float a0, float s,
+                                           const ArrayConsts& ac, int clip_lo, int clip_hi,
+                                           PairSetup& q) {
+    const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const float r2f = (float)R2;
+    const float rinv = rsqrtf(r2f);
+    const float rf = r2f * rinv;
+    const double R = r2f > 1e-30f
+                         ? fma(fma(-(double)rf, (double)rf, R2), 0.5 * (double)rinv, (double)rf)
+                         : sqrt(R2);
+    q.R = R;
     int lo, hi;
+    const float tc = ((float)R * (float)ac.inv_v - (float)ac.t0) * (float)ac.inv_dt;
     if (ac.exact) {
         lo = 0;
         hi = ac.T;
     } else {
-        const double sa = ac.support * (double)a0;
-        const double flo = ceil(((R - sa) * ac.inv_v - ac.t0) * ac.inv_dt);
-        const double fhi = floor(((R + sa) * ac.inv_v - ac.t0) * ac.inv_dt) + 1.0;
-        lo = flo < 0.0 ? 0 : (flo > (double)ac.T ? ac.T : (int)flo);
-        hi = fhi > (double)ac.T ? ac.T : (fhi < 0.0 ? 0 : (int)fhi);
+        const float sa = (float)(ac.support * ac.inv_v * ac.inv_dt) * a0;
+        const float flo = ceilf(tc - sa);
+        const float fhi = floorf(tc + sa) + 1.f;
+        lo = (int)fminf(fmaxf(flo, 0.f), (float)ac.T);
+        hi = (int)fminf(fmaxf(fhi, 0.f), (float)ac.T);
     }
-    g.jlo = lo;
-    g.jhi = hi;
-    double fc = rint((R * ac.inv_v - ac.t0) * ac.inv_dt);
-    int jc = fc < (double)lo ? lo : (fc > (double)(hi - 1) ? hi - 1 : (int)fc);
-    if (hi <= lo) jc = lo;
-    g.jc = jc;
-    const double vt = ac.v * (ac.t0 + (double)jc * ac.dt);
-    g.Dc = (float)(R - vt);
-    g.Uc = (float)(R + vt);
-    const double upmin = R + ac.v * (ac.t0 + (double)lo * ac.dt);
-    g.near = upmin < 10.0 * (double)a0;
+    q.jl = max(lo, clip_lo);
+    q.jh = min(hi, clip_hi);
+    const int rc = __float2int_rn(tc);
+    q.jr = min(max(rc, q.jl), max(q.jh - 1, q.jl));
+    const double vt = fma((double)q.jr, ac.v * ac.dt, ac.v * ac.t0);
+    q.X = (float)(R - vt) * s;
+    q.Y = (float)(R + vt) * s;
+    q.near = (float)R + (float)(ac.v * ac.t0) + (float)(ac.v * ac.dt) * (float)q.jl <
+             10.f * a0;
+}
+
+// Window packing for shared-memory records: jl | jh << 15 | near << 30.
+constexpr int kMaxSamples = 1 << 15;
+__device__ __forceinline__ int pack_window(int jl, int jh, bool near) {
+    return jl | (jh << 15) | (near ? (1 << 30) : 0);
+}
+__device__ __forceinline__ void unpack_window(int w, int& jl, int& jh, bool& near) {
+    jl = w & 0x7fff;
+    jh = (w >> 15) & 0x7fff;
+    near = (w >> 30) & 1;
 }
 
 }  // namespace pc

@@ -17,23 +17,39 @@
 namespace pc {
 
 // ---------------------------------------------------------------- forward
+//
+// CTA = FWD_WARPS sensors x one time segment x one frame (x one ball chunk).
+// Each warp owns one sensor's segment as a private shared-memory trace, so
+// accumulation needs no atomics and its order is fixed (deterministic).
+// Warps never synchronise with each other: each streams the frame's ball
+// records (a compact float4 {x, y, z, a0} cull record, L1/L2 resident) with a
+// one-group prefetch.  Segments are laid over the sensor's ACTIVE arrival
+// range, derived from the frame's ball bounding box, so no segment is empty.
+// Per 32-ball group a lane-parallel fp32 cull drops balls whose +-6 sigma
+// window misses the segment; surviving pairs get the fp64 setup and a 32-byte
+// record; then the warp sweeps each surviving ball's window, lanes on
+// consecutive samples.
 
-constexpr int FWD_WARPS = 4;    // sensors per CTA (one warp owns one sensor)
-constexpr int FWD_TILE = 128;   // balls staged per shared-memory tile
-constexpr int FWD_TSEG_MAX = 2048;
+constexpr int FWD_WARPS = 4;        // warps per forward CTA
+constexpr int FSW = 2;              // sensors per warp (16 lanes each)
+constexpr int FL = 32 / FSW;        // lanes per (ball, sensor) pair
+constexpr int FSTR = 2 * FL;        // samples between a lane's successive pairs
+constexpr int FBATCH = 32 / FSW;    // balls per setup batch (one lane per pair)
+constexpr int FWD_TSEG_MAX = 1024;  // samples per time segment (private traces)
+constexpr int TRACE_PAD = 8;        // floats after a trace (even-window overrun)
 
 struct FwdPlan {
     int Tseg, nseg, nchunk;
     int64_t chunk_balls;
-    size_t partial_bytes, loss_bytes;
+    size_t partial_bytes, loss_bytes, prep_bytes;
 };
 
 static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     FwdPlan p;
     p.Tseg = T < FWD_TSEG_MAX ? ((T + 31) / 32) * 32 : FWD_TSEG_MAX;
     p.nseg = (T + p.Tseg - 1) / p.Tseg;
-    const int64_t tiles = (M + FWD_WARPS - 1) / FWD_WARPS;
-    const int64_t base = (int64_t)p.nseg * tiles * F;
+    const int64_t tiles = (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW);
+    const int64_t base = tiles * F;          // CTAs with work (about one segment each)
     const int64_t want = 6LL * num_sms();
     int64_t c = base >= want ? 1 : (want + base - 1) / base;
     const int64_t cmax = B / 256 > 1 ? B / 256 : 1;
@@ -44,17 +60,97 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     p.partial_bytes = p.nchunk > 1 ? (size_t)p.nchunk * F * M * T * sizeof(float) : 0;
     const int nloss = p.nchunk > 1 ? 1 : p.nseg;
     p.loss_bytes = (size_t)F * M * nloss * sizeof(double);
+    // cull records (F,B) float4 + per-frame bounds (8 u32), 256-byte aligned
+    p.prep_bytes = (((size_t)F * B * sizeof(float4) + 255) / 256) * 256 +
+                   (size_t)F * 8 * sizeof(unsigned);
     return p;
+}
+
+struct FwdWarpSmem {                 // per-warp shared memory
+    float4 rec[32][2];               // pair records of the current batch (lane = pair)
+};
+
+static size_t fwd_smem_bytes(int Tseg) {
+    return (size_t)FWD_WARPS *
+           (sizeof(FwdWarpSmem) + (size_t)FSW * (Tseg + TRACE_PAD) * sizeof(float));
+}
+
+// order-preserving float <-> u32 (atomicMin on the code = float min)
+__device__ __forceinline__ unsigned f2ord(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Per (frame, ball): the float4 cull record, and the frame's bounding box
+// (min xyz, max xyz as ~code, max a0 as ~code: all atomicMin, init 0xff..).
+__global__ void __launch_bounds__(256) k_forward_prep(const double* __restrict__ mu,
+                                                      const float* __restrict__ a0, int64_t B,
+                                                      int F, float4* __restrict__ cull,
+                                                      unsigned* __restrict__ bounds) {
+    const int f = blockIdx.y;
+    unsigned mn[3] = {~0u, ~0u, ~0u}, mxn[4] = {~0u, ~0u, ~0u, ~0u};
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const size_t s = (size_t)f * B + b;
+        const float x = (float)mu[3 * s], y = (float)mu[3 * s + 1], z = (float)mu[3 * s + 2];
+        const float a = a0[s];
+        cull[s] = make_float4(x, y, z, a);
+        const float v[3] = {x, y, z};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            mn[k] = min(mn[k], f2ord(v[k]));
+            mxn[k] = min(mxn[k], ~f2ord(v[k]));
+        }
+        mxn[3] = min(mxn[3], ~f2ord(a));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            mn[k] = min(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mxn[k] = min(mxn[k], __shfl_xor_sync(0xffffffffu, mxn[k], o));
+        }
+        mxn[3] = min(mxn[3], __shfl_xor_sync(0xffffffffu, mxn[3], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        unsigned* bf = bounds + 8 * f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            atomicMin(bf + k, mn[k]);
+            atomicMin(bf + 3 + k, mxn[k]);
+        }
+        atomicMin(bf + 6, mxn[3]);
+    }
+}
+
+// Can the Gaussian-on-grid recurrence run for this ball?  x starts at most
+// ~support*sqrt(log2 e / 2) + 2 vs from the wavefront; the ratios g (and the
+// second ratio h = 2^-2D^2, D = stride * vs) must stay inside fp32's range.
+__device__ __forceinline__ bool recur_ok(float D, float vs, float support) {
+    const float xmax = sqrtf(kHalfLog2e) * support + 2.f * vs;
+    return 2.f * D * xmax + D * D <= 120.f && 2.f * D * D <= 120.f;
+}
+
+// Per-lane start of the recurrence for samples (j, j+1): e = 2^-x^2,
+// g = e(j + stride) / e(j) = 2^(2 D x - D^2).
+__device__ __forceinline__ void recur_init(float2 x, float D, float2& e, float2& g) {
+    e = ex2n_2(fmul2(x, x));
+    g = ex2_2(ffma2(x, splat2(2.f * D), splat2(-D * D)));
 }
 
 struct FwdArgs {
     const double* mu;
-    const float* a0;
     const float* p0;
+    const float4* cull;
+    const unsigned* bounds;
     const double* pos;
+    const int* sorder;   // sensor processing order (spatial neighbours) or NULL
     const float* obs;
-    float* out;       // final (nchunk == 1) or partial traces (nchunk > 1)
-    double* loss;     // (F, M, nseg) partials or NULL
+    float* out;          // final (nchunk == 1) or partial traces (nchunk > 1)
+    double* loss;        // (F, M, nseg) partials or NULL
     long long* coinc;
     int64_t B;
     int F, M;
@@ -63,133 +159,229 @@ struct FwdArgs {
     int64_t chunk_balls;
 };
 
-template <bool NEAR>
-__device__ __forceinline__ void fwd_window(float* __restrict__ tr, int s0, int jl, int jh, int jc,
-                                           float Dc, float Uc, float c, float nk, float vdt,
-                                           int lane) {
-    int j = jl + lane;
-    float kf = (float)(j - jc);
-    for (; j < jh; j += 32, kf += 32.f) {
-        const float um = fmaf(-kf, vdt, Dc);
-        float val = um * ex2(um * um * nk);
-        if (NEAR) {
-            const float up = fmaf(kf, vdt, Uc);
-            val = fmaf(up, ex2(up * up * nk), val);
+// Record of one (ball, sensor) pair, written by its setup lane:
+//   r0 = {je0, niter | near << 30, X0, c}   X0 = s (R - v t_je0), or X at jr (exact)
+//   r1 = {vs, Y0, span = je1 - je0, jr}
+// niter = 0 marks an empty pair.
+
+// Both half-warps sweep the same ball for their own sensor: lane `sub` of a
+// half owns sample pairs (j, j+1), j = je0 + 2 sub + FSTR n, so each half's
+// float2 access is 128 contiguous bytes of its own trace (one conflict-free
+// wavefront).  Trip counts of the two halves differ by at most one; the loop
+// runs the larger with per-lane predication.
+template <bool EXACT>
+__device__ __forceinline__ void fwd_sweep2(float* __restrict__ tr, float4 r0, float4 r1,
+                                           float2 sub2, int sub) {
+    const int je0 = __float_as_int(r0.x);
+    const int wn = __float_as_int(r0.y);
+    const int nl = wn & 0x3fffffff;
+    const bool near = (wn >> 30) & 1;
+    const int nmax = max(nl, __shfl_xor_sync(0xffffffffu, nl, FL));
+    if (nmax == 0) return;
+    const int span = __float_as_int(r1.z) - 2 * sub;
+    const float2 cc = splat2(r0.w);
+    const float vs = r1.x;
+    float2* p = reinterpret_cast<float2*>(tr + je0) + sub;
+    const bool anynear = __any_sync(0xffffffffu, near && nl > 0);
+    if (!EXACT && !anynear) {
+        float2 x = ffma2(sub2, splat2(-vs), splat2(r0.z));
+        const float2 dx = splat2(-(float)FSTR * vs);
+#pragma unroll 4
+        for (int n = 0; n < nmax; ++n, p += FL) {
+            const float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
+            if (FSTR * n < span) *p = ffma2(cc, v, *p);
+            x = fadd2(x, dx);
         }
-        tr[j - s0] = fmaf(c, val, tr[j - s0]);
+    } else {
+        // exact / near field: x (and y) from the exact integer offset to the
+        // reference sample (r1.w) every iteration; r0.z / r1.y are X / Y there
+        const int jr = __float_as_int(r1.w);
+        const float Xr = EXACT ? r0.z : fmaf((float)(je0 - jr), vs, r0.z);   // X at jr
+        const float Yr = r1.y;                                               // Y at jr
+        float2 k = fadd2(sub2, splat2((float)(je0 - jr)));
+        for (int n = 0; n < nmax; ++n, p += FL) {
+            const float2 x = ffma2(k, splat2(-vs), splat2(Xr));
+            float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
+            if (near) {
+                const float2 y = ffma2(k, splat2(vs), splat2(Yr));
+                v = ffma2(y, ex2n_2(fmul2(y, y)), v);
+            }
+            if (FSTR * n < span) *p = ffma2(cc, v, *p);
+            k = fadd2(k, splat2((float)FSTR));
+        }
     }
 }
 
+// CTA = FWD_WARPS warps x FSW neighbouring sensors each, one time segment,
+// one frame (x one ball chunk); no CTA-wide synchronisation.  Each sensor has
+// a private shared-memory trace over the segment, laid over the warp's active
+// arrival range (frame bounding box); for the BASELINE scenes one segment
+// holds the whole range, so every pair is set up and swept exactly once.
+// Per batch of 16 balls the 32 lanes set up the 16 x 2 pairs (fp32 cull,
+// fp64 geometry) into shared-memory records; then both half-warps sweep each
+// surviving ball for their own sensor (fixed ball order: deterministic).
+template <bool EXACT>
 __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* smx = reinterpret_cast<double*>(smem);
-    double* smy = smx + FWD_TILE;
-    double* smz = smy + FWD_TILE;
-    float* sa0 = reinterpret_cast<float*>(smz + FWD_TILE);
-    float* sp0 = sa0 + FWD_TILE;
-    float* traces = sp0 + FWD_TILE;
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TP = a.Tseg + TRACE_PAD;
+    FwdWarpSmem& ws = reinterpret_cast<FwdWarpSmem*>(smem)[warp];
+    float* traces = reinterpret_cast<float*>(reinterpret_cast<FwdWarpSmem*>(smem) + FWD_WARPS) +
+                    warp * FSW * TP;
     const int seg = blockIdx.x % a.nseg;
     const int chunk = blockIdx.x / a.nseg;
-    const int m = blockIdx.y * FWD_WARPS + warp;
     const int f = blockIdx.z;
     const int T = a.ac.T;
-    const int s0 = seg * a.Tseg;
-    const int s1 = min(T, s0 + a.Tseg);
-    const bool active = m < a.M;
-    float* tr = traces + warp * a.Tseg;
-    for (int j = lane; j < a.Tseg; j += 32) tr[j] = 0.f;
+    const int slot0 = (blockIdx.y * FWD_WARPS + warp) * FSW;
+    if (slot0 >= a.M) return;
+    const int h = lane / FL, sub = lane % FL;      // half = sensor slot
+    const int slot = slot0 + h;
+    const int m = slot < a.M ? (a.sorder ? a.sorder[slot] : slot) : -1;
 
     double px = 0.0, py = 0.0, pz = 0.0;
-    if (active) {
+    if (m >= 0) {
         px = a.pos[3 * m + 0];
         py = a.pos[3 * m + 1];
         pz = a.pos[3 * m + 2];
     }
+    const float fpx = (float)px, fpy = (float)py, fpz = (float)pz;
+    const float sup = (float)a.ac.support;
+
+    // ---- active arrival range (union over the warp's sensors)
+    int act_lo = 0, act_hi = T;
+    float dmin_box = 0.f;
+    if (!EXACT) {
+        const unsigned* bf = a.bounds + 8 * f;
+        const float lx = ord2f(bf[0]), ly = ord2f(bf[1]), lz = ord2f(bf[2]);
+        const float hx = ord2f(~bf[3]), hy = ord2f(~bf[4]), hz = ord2f(~bf[5]);
+        const float amax = ord2f(~bf[6]);
+        const float nx = fmaxf(fmaxf(lx - fpx, fpx - hx), 0.f);
+        const float ny = fmaxf(fmaxf(ly - fpy, fpy - hy), 0.f);
+        const float nz = fmaxf(fmaxf(lz - fpz, fpz - hz), 0.f);
+        const float fx = fmaxf(fabsf(lx - fpx), fabsf(hx - fpx));
+        const float fy = fmaxf(fabsf(ly - fpy), fabsf(hy - fpy));
+        const float fz = fmaxf(fabsf(lz - fpz), fabsf(hz - fpz));
+        float dmin = sqrtf(nx * nx + ny * ny + nz * nz);
+        float dmax = sqrtf(fx * fx + fy * fy + fz * fz);
+        if (m < 0) {
+            dmin = 3.4e38f;
+            dmax = 0.f;
+        }
+        dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, FL));
+        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, FL));
+        dmin_box = dmin;
+        const float w = sup * amax;
+        const double tlo = (((double)dmin - w) * a.ac.inv_v - a.ac.t0) * a.ac.inv_dt;
+        const double thi = (((double)dmax + w) * a.ac.inv_v - a.ac.t0) * a.ac.inv_dt;
+        const double pad = 2.0 + 1e-5 * (double)dmax * a.ac.inv_v * a.ac.inv_dt;
+        act_lo = (int)fmax(0.0, fmin((double)T, floor(tlo - pad)));
+        act_hi = (int)fmax((double)act_lo, fmin((double)T, ceil(thi + pad)));
+    }
+    act_lo &= ~1;                                   // even segment starts
+    const int nseg_w = max(1, (act_hi - act_lo + a.Tseg - 1) / a.Tseg);
+    if (seg >= nseg_w) {
+        if (a.loss && a.nchunk == 1 && sub == 0 && m >= 0)
+            a.loss[((size_t)f * a.M + m) * a.nseg + seg] = 0.0;
+        return;
+    }
+    const int s0 = act_lo + seg * a.Tseg;           // ball-active part of the segment
+    const int s1 = min(act_hi, s0 + a.Tseg);
+    const int w0 = seg == 0 ? 0 : s0;               // output range this warp writes
+    const int w1 = seg == nseg_w - 1 ? T : s1;
+    for (int j = lane; j < FSW * TP; j += 32) traces[j] = 0.f;
+    float* tr = traces + h * TP - s0;               // this half's sensor, absolute index
+
+    const float d_lo = (float)(a.ac.v * (a.ac.t0 + (double)s0 * a.ac.dt)) - 2.f * a.ac.vdt;
+    const float d_hi = (float)(a.ac.v * (a.ac.t0 + (double)(s1 - 1) * a.ac.dt)) + 2.f * a.ac.vdt;
     const int64_t b0 = (int64_t)chunk * a.chunk_balls;
     const int64_t b1 = min(a.B, b0 + a.chunk_balls);
     const size_t fb = (size_t)f * a.B;
+    const float4* cl = a.cull + fb;
     const float vdt = a.ac.vdt;
+    const bool scan = s1 > s0 || (seg == 0 && dmin_box < 1e-3f);
+    const float2 sub2 = make_float2((float)(2 * sub), (float)(2 * sub + 1));
+    __syncwarp();
 
-    for (int64_t tb = b0; tb < b1; tb += FWD_TILE) {
-        const int n_in = (int)min((int64_t)FWD_TILE, b1 - tb);
-        __syncthreads();
-        for (int i = threadIdx.x; i < n_in; i += blockDim.x) {
-            const size_t s = fb + tb + i;
-            smx[i] = a.mu[3 * s + 0];
-            smy[i] = a.mu[3 * s + 1];
-            smz[i] = a.mu[3 * s + 2];
-            sa0[i] = a.a0[s];
-            sp0[i] = a.p0[s];
-        }
-        __syncthreads();
-        if (!active) continue;
-        for (int g = 0; g < n_in; g += 32) {
-            const int i = g + lane;
-            bool valid = i < n_in;
-            int jl = 0, jh = 0, jc = 0, near = 0;
-            float Dc = 0.f, Uc = 0.f, c = 0.f, nk = 0.f;
-            if (valid) {
-                const float av = sa0[i];
-                PairGeom pg;
-                pair_geometry(smx[i] - px, smy[i] - py, smz[i] - pz, av, a.ac, pg);
-                if (pg.R < kCoincidenceEps) {
-                    atomicMin(a.coinc, (long long)(tb + i) * a.M + m);
-                    valid = false;
+    if (scan) {
+        float4 nxt = b0 + sub < b1 ? cl[b0 + sub] : make_float4(0.f, 0.f, 0.f, 1.f);
+        for (int64_t g = b0; g < b1; g += FBATCH) {
+            const float4 cur = nxt;
+            const int64_t i = g + sub;                  // this lane's ball (sensor h)
+            if (g + FBATCH + sub < b1) nxt = cl[g + FBATCH + sub];
+            bool pass = false;
+            if (i < b1 && m >= 0) {
+                const float dx = cur.x - fpx, dy = cur.y - fpy, dz = cur.z - fpz;
+                const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                const float w = sup * cur.w + 1e-5f * r;
+                pass = EXACT || r < 1e-3f || (r + w >= d_lo && r - w <= d_hi);
+            }
+            float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+            if (pass) {
+                const float av = cur.w;
+                const float s = scale_of(av);
+                const size_t q3 = 3 * (fb + i);
+                PairSetup q;
+                pair_setup(a.mu[q3] - px, a.mu[q3 + 1] - py, a.mu[q3 + 2] - pz, av, s, a.ac, s0,
+                           s1, q);
+                if (q.R < kCoincidenceEps) {
+                    atomicMin(a.coinc, (long long)i * a.M + m);
+                    pass = false;
+                } else if (q.jh <= q.jl) {
+                    pass = false;
                 } else {
-                    jl = max(pg.jlo, s0);
-                    jh = min(pg.jhi, s1);
-                    valid = jh > jl;
-                    jc = pg.jc;
-                    Dc = pg.Dc;
-                    Uc = pg.Uc;
-                    near = pg.near;
-                    c = sp0[i] * (0.5f / (float)pg.R);
-                    nk = -0.5f * kLog2e / (av * av);
+                    const float c = __fdividef(0.5f * __ldg(a.p0 + fb + i), (float)q.R * s);
+                    const float vs = vdt * s;
+                    const int je0 = q.jl & ~1;
+                    const int span = ((q.jh + 1) & ~1) - je0;
+                    const int niter = (span + FSTR - 1) / FSTR;
+                    const float X0 = EXACT ? q.X : fmaf((float)(q.jr - je0), vs, q.X);
+                    q0 = make_float4(__int_as_float(je0),
+                                     __int_as_float(niter | (q.near ? 1 << 30 : 0)), X0, c);
+                    q1 = make_float4(vs, q.Y, __int_as_float(span), __int_as_float(q.jr));
                 }
             }
-            unsigned mask = __ballot_sync(0xffffffffu, valid);
+            ws.rec[lane][0] = q0;
+            ws.rec[lane][1] = q1;
+            const unsigned pm = __ballot_sync(0xffffffffu, pass);
+            unsigned mask = (pm | (pm >> FL)) & ((1u << FL) - 1u);   // balls with any pair
+            __syncwarp();
             while (mask) {
-                const int src = __ffs(mask) - 1;
+                const int b = __ffs(mask) - 1;
                 mask &= mask - 1;
-                const int bjl = __shfl_sync(0xffffffffu, jl, src);
-                const int bjh = __shfl_sync(0xffffffffu, jh, src);
-                const int bjc = __shfl_sync(0xffffffffu, jc, src);
-                const int bnear = __shfl_sync(0xffffffffu, near, src);
-                const float bDc = __shfl_sync(0xffffffffu, Dc, src);
-                const float bc = __shfl_sync(0xffffffffu, c, src);
-                const float bnk = __shfl_sync(0xffffffffu, nk, src);
-                if (bnear) {
-                    const float bUc = __shfl_sync(0xffffffffu, Uc, src);
-                    fwd_window<true>(tr, s0, bjl, bjh, bjc, bDc, bUc, bc, bnk, vdt, lane);
-                } else {
-                    fwd_window<false>(tr, s0, bjl, bjh, bjc, bDc, 0.f, bc, bnk, vdt, lane);
-                }
+                const int src = h * FL + b;
+                fwd_sweep2<EXACT>(tr, ws.rec[src][0], ws.rec[src][1], sub2, sub);
+                __syncwarp();
             }
         }
     }
     __syncwarp();
-    if (!active) return;
-    const size_t row = ((size_t)f * a.M + m) * T;
-    if (a.nchunk > 1) {
-        float* dst = a.out + (size_t)chunk * a.F * a.M * T + row;
-        for (int j = s0 + lane; j < s1; j += 32) dst[j] = tr[j - s0];
-        return;
-    }
-    double lsum = 0.0;
-    if (a.obs) {
-        for (int j = s0 + lane; j < s1; j += 32) {
-            const float r = tr[j - s0] - __ldg(a.obs + row + j);
-            a.out[row + j] = r;
-            lsum = fma((double)r, (double)r, lsum);
+    // ---- epilogue: each sensor of the warp, written by the whole warp
+    for (int hh = 0; hh < FSW; ++hh) {
+        const int mq = __shfl_sync(0xffffffffu, m, hh * FL);
+        if (mq < 0) continue;
+        const float* tq = traces + hh * TP - s0;
+        const size_t row = ((size_t)f * a.M + mq) * T;
+        if (a.nchunk > 1) {
+            float* dst = a.out + (size_t)chunk * a.F * a.M * T + row;
+            for (int j = w0 + lane; j < w1; j += 32) dst[j] = (j >= s0 && j < s1) ? tq[j] : 0.f;
+            continue;
         }
-    } else {
-        for (int j = s0 + lane; j < s1; j += 32) a.out[row + j] = tr[j - s0];
-    }
-    if (a.loss) {
-        lsum = warp_sum(lsum);
-        if (lane == 0) a.loss[((size_t)f * a.M + m) * a.nseg + seg] = lsum;
+        double lsum = 0.0;
+        if (a.obs) {
+            for (int j = w0 + lane; j < w1; j += 32) {
+                const float pv = (j >= s0 && j < s1) ? tq[j] : 0.f;
+                const float r = pv - __ldg(a.obs + row + j);
+                a.out[row + j] = r;
+                lsum = fma((double)r, (double)r, lsum);
+            }
+        } else {
+            for (int j = w0 + lane; j < w1; j += 32)
+                a.out[row + j] = (j >= s0 && j < s1) ? tq[j] : 0.f;
+        }
+        if (a.loss) {
+            lsum = warp_sum(lsum);
+            if (lane == 0) a.loss[((size_t)f * a.M + mq) * a.nseg + seg] = lsum;
+        }
     }
 }
 
@@ -242,8 +434,24 @@ __global__ void __launch_bounds__(256) k_loss_reduce(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------- adjoint
+//
+// One warp owns one (ball, frame).  Per block of 32 sensors the lanes form the
+// pair setups in parallel (fp64) into 48-byte shared-memory records; then
+// lane groups of LG lanes take one pair each (NGRP pairs at a time).  Each
+// lane owns sample pairs (j, j+1) of the pair's even-extended window, reads
+// them with one 64-bit load and accumulates three scaled partial sums with
+// packed fp32x2 arithmetic:
+//   A1 = sum r e x,  AQ = sum r e (1 - kappa x^2),  A3 = sum r e x^3,
+// e = 2^-x^2 from the recurrence e <- e g, g <- g h (MUFU only at the start;
+// the near-field and exact paths use one MUFU per term and sample).  Every
+// pair constant multiplies a lane-local partial, so the per-pair reduction is
+// deferred: lanes fold their partials into five ball accumulators and the
+// warp reduces once per ball (fixed xor order: deterministic).
 
-constexpr int ADJ_WARPS = 4;  // balls per CTA (one warp owns one (ball, frame))
+constexpr int ADJ_WARPS = 4;      // balls per CTA
+constexpr int LG = 4;             // lanes per pair (adjoint)
+constexpr int NGRP = 32 / LG;     // pairs in flight per warp
+constexpr int LSTRIDE = 2 * LG;   // samples between a lane's successive pairs
 
 struct AdjArgs {
     const double* mu;
@@ -258,35 +466,28 @@ struct AdjArgs {
     ArrayConsts ac;
 };
 
-enum { REC_VALID = 1, REC_NEAR = 2 };
-
-// One pair's partial sums over the samples this lane owns.
-template <int G, bool NEAR>
-__device__ __forceinline__ void adj_window(const float* __restrict__ row, int j, int jh, float kf,
-                                           float Dc, float Uc, float nk, float inv_a2, float vdt,
-                                           float& A1, float& AQ, float& A3) {
-    for (; j < jh; j += G, kf += (float)G) {
-        const float r = __ldg(row + j);
-        const float um = fmaf(-kf, vdt, Dc);
-        const float u2 = um * um;
-        const float w = r * ex2(u2 * nk);
-        A1 = fmaf(w, um, A1);
-        AQ = fmaf(w, fmaf(u2, -inv_a2, 1.f), AQ);
-        A3 = fmaf(w * u2, um, A3);
-        if (NEAR) {
-            const float up = fmaf(kf, vdt, Uc);
-            const float p2 = up * up;
-            const float wp = r * ex2(p2 * nk);
-            A1 = fmaf(wp, up, A1);
-            AQ = fmaf(wp, fmaf(p2, -inv_a2, 1.f), AQ);
-            A3 = fmaf(wp * p2, up, A3);
-        }
-    }
+template <bool ALIGNED>
+__device__ __forceinline__ float2 load_pair(const float* __restrict__ row, int j, int T) {
+    if (ALIGNED) return __ldg(reinterpret_cast<const float2*>(row + j));
+    return make_float2(__ldg(row + j), j + 1 < T ? __ldg(row + j + 1) : 0.f);
 }
 
-template <int G>
+// Sample-pair moments A0 = sum w, A1 = sum w x, A2 = sum w x^2, A3 = sum w x^3
+// (w = r e); AQ = A0 - kappa A2 is formed once per pair.  7 packed ops.
+__device__ __forceinline__ void accum_pair(float2 r, float2 e, float2 x, float2& A0, float2& A1,
+                                           float2& A2, float2& A3) {
+    const float2 w = fmul2(r, e);
+    A0 = fadd2(A0, w);
+    const float2 t = fmul2(w, x);
+    A1 = fadd2(A1, t);
+    const float2 u = fmul2(t, x);
+    A2 = fadd2(A2, u);
+    A3 = ffma2(u, x, A3);
+}
+
+template <bool ALIGNED>
 __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
-    __shared__ __align__(16) float4 recs[ADJ_WARPS][32][4];
+    __shared__ __align__(16) float4 recs[ADJ_WARPS][32][3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * ADJ_WARPS + warp;
     const int f = blockIdx.y;
@@ -294,74 +495,137 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     const size_t sb = (size_t)f * a.B + b;
     const double mx = a.mu[3 * sb + 0], my = a.mu[3 * sb + 1], mz = a.mu[3 * sb + 2];
     const float av = a.a0[sb], pv = a.p0[sb];
-    const float inv_a2 = 1.f / (av * av);
-    const float nk = -0.5f * kLog2e * inv_a2;
-    const float vdt = a.ac.vdt;
+    const float s = scale_of(av);
+    const float vs = a.ac.vdt * s;
+    const float inv_s = 1.f / s;
+    const float ka_ball = pv / (av * av * av) * inv_s * inv_s * inv_s;
     const int T = a.ac.T;
+    const float D = (float)LSTRIDE * vs;
+    const bool fast = !a.ac.exact && recur_ok(D, vs, (float)a.ac.support);
+    const float2 h2 = splat2(ex2(-2.f * D * D));
+    const float2 mD2 = splat2(-D);
+    const float2 mvs2 = splat2(-vs);
+    const float2 vs2 = splat2(vs);
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f;
-    float4(&rec)[32][4] = recs[warp];
+    float4(&rec)[32][3] = recs[warp];
+    const int grp = lane / LG, sub = lane % LG;
 
     for (int mb = 0; mb < a.M; mb += 32) {
         const int m = mb + lane;
-        int flags = 0;
-        PairGeom pg;
-        pg.jlo = pg.jhi = pg.jc = 0;
-        pg.Dc = pg.Uc = 0.f;
-        pg.R = 1.0;
+        int win = 0, jr = 0;
+        float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
         float ux = 0.f, uy = 0.f, uz = 0.f;
         if (m < a.M) {
             const double dx = mx - a.pos[3 * m + 0];
             const double dy = my - a.pos[3 * m + 1];
             const double dz = mz - a.pos[3 * m + 2];
-            pair_geometry(dx, dy, dz, av, a.ac, pg);
-            if (pg.R < kCoincidenceEps) {
+            PairSetup q;
+            pair_setup(dx, dy, dz, av, s, a.ac, 0, T, q);
+            if (q.R < kCoincidenceEps) {
                 atomicMin(a.coinc, (long long)b * a.M + m);
-            } else {
-                flags = (pg.jhi > pg.jlo ? REC_VALID : 0) | (pg.near ? REC_NEAR : 0);
-                const double ir = 1.0 / pg.R;
+            } else if (q.jh > q.jl) {
+                win = pack_window(q.jl, q.jh, q.near);
+                jr = q.jr;
+                X = q.X;
+                Y = q.Y;
+                const double ir = 1.0 / q.R;
+                const float inv2R = (float)(0.5 * ir);
+                kp = inv2R * inv_s;
+                ka = ka_ball * inv2R;
+                kR2 = pv * inv2R;
+                kR1 = -kR2 * (float)ir * inv_s;
                 ux = (float)(dx * ir);
                 uy = (float)(dy * ir);
                 uz = (float)(dz * ir);
             }
         }
-        const float inv2R = (float)(0.5 / pg.R);
-        const float kp = inv2R;
-        const float ka = pv * inv2R * inv_a2 / av;
-        const float kR2 = pv * inv2R;
-        const float kR1 = -kR2 * (float)(1.0 / pg.R);
-        rec[lane][0] = make_float4(__int_as_float(pg.jlo), __int_as_float(pg.jhi),
-                                   __int_as_float(pg.jc), __int_as_float(flags));
-        rec[lane][1] = make_float4(pg.Dc, pg.Uc, kp, ka);
-        rec[lane][2] = make_float4(kR1, kR2, ux, uy);
-        rec[lane][3] = make_float4(uz, 0.f, 0.f, 0.f);
+        rec[lane][0] = make_float4(__int_as_float(win), __int_as_float(jr), X, kp);
+        rec[lane][1] = make_float4(ka, kR1, kR2, ux);
+        rec[lane][2] = make_float4(uy, uz, Y, 0.f);
         __syncwarp();
         const int npair = min(32, a.M - mb);
-        for (int pb = 0; pb < npair; pb += 32 / G) {
-            const int pi = pb + lane / G;
-            const int s = lane % G;
+        for (int pb = 0; pb < npair; pb += NGRP) {
+            const int pi = pb + grp;
+            if (pi >= npair) continue;
             const float4 r0 = rec[pi][0];
-            const int rflags = __float_as_int(r0.w);
-            if (pi < npair && (rflags & REC_VALID)) {
-                const float4 r1 = rec[pi][1];
-                const int jl = __float_as_int(r0.x), jh = __float_as_int(r0.y);
-                const int jc = __float_as_int(r0.z);
-                const float* row = a.resid + ((size_t)f * a.M + mb + pi) * T;
-                float A1 = 0.f, AQ = 0.f, A3 = 0.f;
-                const int j = jl + s;
-                const float kf = (float)(j - jc);
-                if (rflags & REC_NEAR)
-                    adj_window<G, true>(row, j, jh, kf, r1.x, r1.y, nk, inv_a2, vdt, A1, AQ, A3);
-                else
-                    adj_window<G, false>(row, j, jh, kf, r1.x, 0.f, nk, inv_a2, vdt, A1, AQ, A3);
-                const float4 r2 = rec[pi][2];
-                const float4 r3 = rec[pi][3];
-                const float accR = fmaf(r2.x, A1, r2.y * AQ);
-                g0 = fmaf(r1.w, A3, g0);
-                g1 = fmaf(r1.z, A1, g1);
-                g2 = fmaf(accR, r2.z, g2);
-                g3 = fmaf(accR, r2.w, g3);
-                g4 = fmaf(accR, r3.x, g4);
+            const int w = __float_as_int(r0.x);
+            if (w == 0) continue;
+            int jl, jh;
+            bool near;
+            unpack_window(w, jl, jh, near);
+            const int je1 = (jh + 1) & ~1;
+            int j = (jl & ~1) + 2 * sub;
+            const float* row = a.resid + ((size_t)f * a.M + mb + pi) * T;
+            float2 A0 = splat2(0.f), A1 = A0, A2 = A0, A3 = A0;
+            if (j < je1) {
+                const int jrr = __float_as_int(r0.y);
+                float2 k = make_float2((float)(j - jrr), (float)(j + 1 - jrr));
+                float2 x = ffma2(k, mvs2, splat2(r0.z));
+                if (fast && !near) {
+                    float2 e, g;
+                    recur_init(x, D, e, g);
+                    int n = (je1 - j + LSTRIDE - 1) / LSTRIDE;   // sample pairs of this lane
+                    if (ALIGNED) {
+                        // software-pipelined: the next 4 sample pairs are in
+                        // flight while the current 4 are accumulated
+                        const float2* p = reinterpret_cast<const float2*>(row + j);
+                        float2 nx[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            nx[u] = u < n ? __ldg(p + u * LG) : splat2(0.f);
+                        while (n > 0) {
+                            float2 cr[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) cr[u] = nx[u];
+                            const int nc = n;
+                            p += 4 * LG;
+                            n -= 4;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                nx[u] = u < n ? __ldg(p + u * LG) : splat2(0.f);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                if (u < nc) {
+                                    accum_pair(cr[u], e, x, A0, A1, A2, A3);
+                                    e = fmul2(e, g);
+                                    g = fmul2(g, h2);
+                                    x = fadd2(x, mD2);
+                                }
+                            }
+                        }
+                    } else {
+                        for (; j < je1; j += LSTRIDE) {
+                            accum_pair(load_pair<ALIGNED>(row, j, T), e, x, A0, A1, A2, A3);
+                            e = fmul2(e, g);
+                            g = fmul2(g, h2);
+                            x = fadd2(x, mD2);
+                        }
+                    }
+                } else {
+                    const float Yr = rec[pi][2].z;
+                    const float2 kstep = splat2((float)LSTRIDE);
+                    for (; j < je1; j += LSTRIDE) {
+                        const float2 r = load_pair<ALIGNED>(row, j, T);
+                        x = ffma2(k, mvs2, splat2(r0.z));
+                        accum_pair(r, ex2n_2(fmul2(x, x)), x, A0, A1, A2, A3);
+                        if (near) {
+                            const float2 y = ffma2(k, vs2, splat2(Yr));
+                            accum_pair(r, ex2n_2(fmul2(y, y)), y, A0, A1, A2, A3);
+                        }
+                        k = fadd2(k, kstep);
+                    }
+                }
             }
+            const float a1 = A1.x + A1.y, a3 = A3.x + A3.y;
+            const float aq = fmaf(A2.x + A2.y, -kKappa, A0.x + A0.y);
+            const float4 r1 = rec[pi][1];
+            const float4 r2 = rec[pi][2];
+            const float accR = fmaf(r1.y, a1, r1.z * aq);
+            g0 = fmaf(r1.x, a3, g0);
+            g1 = fmaf(r0.w, a1, g1);
+            g2 = fmaf(accR, r1.w, g2);
+            g3 = fmaf(accR, r2.x, g3);
+            g4 = fmaf(accR, r2.y, g4);
         }
         __syncwarp();
     }
@@ -410,15 +674,16 @@ extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array
     plan[0] = p.Tseg;
     plan[1] = p.nseg;
     plan[2] = p.nchunk;
-    plan[3] = 2 + (p.nchunk > 1 ? 1 : 0);  // forward [+ combine] + loss reduce
+    plan[3] = 3 + (p.nchunk > 1 ? 1 : 0);  // prep + forward [+ combine] + loss reduce
     return PC_OK;
 }
 
 extern "C" size_t pc_forward_workspace_bytes(int64_t n_balls, int32_t n_frames,
                                              const pc_array_t* array) {
     if (!array || n_balls < 0 || n_frames < 1) return 0;
-    FwdPlan p = fwd_plan(n_balls, n_frames, array->n_sensors, array->n_samples);
-    return p.partial_bytes + p.loss_bytes + 256;
+    FwdPlan p = fwd_plan(n_balls > 0 ? n_balls : 1, n_frames, array->n_sensors,
+                         array->n_samples);
+    return p.prep_bytes + p.partial_bytes + p.loss_bytes + 256;
 }
 
 extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const float* p0_t,
@@ -429,23 +694,36 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
     ArrayConsts ac;
     if (!array_consts(array, ac) || n_balls < 0 || n_frames < 1 || !out || !coincident)
         return PC_ERR_ARGUMENT;
+    if (array->n_samples >= kMaxSamples) return PC_ERR_UNSUPPORTED;
     const int M = array->n_sensors, T = array->n_samples, F = n_frames;
     cudaStream_t st = as_stream(stream);
     if (n_balls > 0 && (!mu_t || !a0_t || !p0_t)) return PC_ERR_ARGUMENT;
     FwdPlan p = fwd_plan(n_balls > 0 ? n_balls : 1, F, M, T);
-    const size_t need = p.partial_bytes + p.loss_bytes;
-    if (need > 0 && (!workspace || workspace_bytes < need)) return PC_ERR_ARGUMENT;
+    const size_t need = p.partial_bytes + p.loss_bytes + p.prep_bytes;
+    if (!workspace || workspace_bytes < need) return PC_ERR_ARGUMENT;
     unsigned char* ws = static_cast<unsigned char*>(workspace);
-    float* partial = p.partial_bytes ? reinterpret_cast<float*>(ws) : nullptr;
-    double* lpart = reinterpret_cast<double*>(ws + p.partial_bytes);
+    float4* cull = reinterpret_cast<float4*>(ws);
+    unsigned* bounds = reinterpret_cast<unsigned*>(
+        ws + (((size_t)F * (n_balls > 0 ? n_balls : 1) * sizeof(float4) + 255) / 256) * 256);
+    unsigned char* rest = ws + p.prep_bytes;
+    float* partial = p.partial_bytes ? reinterpret_cast<float*>(rest) : nullptr;
+    double* lpart = reinterpret_cast<double*>(rest + p.partial_bytes);
     const bool want_loss = observed && loss_per_frame;
 
     if (n_balls > 0) {
+        if (cudaMemsetAsync(bounds, 0xff, (size_t)F * 8 * sizeof(unsigned), st) != cudaSuccess)
+            return PC_ERR_CUDA;
+        int64_t pb = (n_balls + 255) / 256;
+        if (pb > 2LL * num_sms()) pb = 2LL * num_sms();
+        k_forward_prep<<<dim3((unsigned)pb, F), 256, 0, st>>>(mu_t, a0_t, n_balls, F, cull,
+                                                              bounds);
         FwdArgs a;
         a.mu = mu_t;
-        a.a0 = a0_t;
         a.p0 = p0_t;
+        a.cull = cull;
+        a.bounds = bounds;
         a.pos = array->positions;
+        a.sorder = array->sensor_order;
         a.obs = observed;
         a.out = p.nchunk > 1 ? partial : out;
         a.loss = (want_loss && p.nchunk == 1) ? lpart : nullptr;
@@ -458,16 +736,19 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         a.nseg = p.nseg;
         a.nchunk = p.nchunk;
         a.chunk_balls = p.chunk_balls;
-        const size_t smem = (size_t)FWD_TILE * (3 * sizeof(double) + 2 * sizeof(float)) +
-                            (size_t)FWD_WARPS * p.Tseg * sizeof(float);
+        const size_t smem = fwd_smem_bytes(p.Tseg);
         static bool attr_set = false;
         if (!attr_set) {
-            cudaFuncSetAttribute(k_forward, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 64 * 1024);
+            const int mx = (int)fwd_smem_bytes(FWD_TSEG_MAX);
+            cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             attr_set = true;
         }
-        dim3 grid(p.nseg * p.nchunk, (M + FWD_WARPS - 1) / FWD_WARPS, F);
-        k_forward<<<grid, FWD_WARPS * 32, smem, st>>>(a);
+        dim3 grid(p.nseg * p.nchunk, (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW), F);
+        if (ac.exact)
+            k_forward<true><<<grid, FWD_WARPS * 32, smem, st>>>(a);
+        else
+            k_forward<false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         if (p.nchunk > 1) {
             k_forward_finish<<<dim3(M, F), 256, 0, st>>>(partial, observed, out,
                                                         want_loss ? lpart : nullptr, p.nchunk,
@@ -495,6 +776,7 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     ArrayConsts ac;
     if (!array_consts(array, ac) || n_balls < 0 || n_frames < 1 || !coincident)
         return PC_ERR_ARGUMENT;
+    if (array->n_samples >= kMaxSamples) return PC_ERR_UNSUPPORTED;
     if (n_balls == 0) return PC_OK;
     if (!mu_t || !a0_t || !p0_t || !residual || !G) return PC_ERR_ARGUMENT;
     AdjArgs a;
@@ -511,7 +793,9 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     a.ac = ac;
     dim3 grid((unsigned)((n_balls + ADJ_WARPS - 1) / ADJ_WARPS), n_frames);
     cudaStream_t st = as_stream(stream);
-    // lane-group width per pair from the typical window length 12 a0 / (v dt)
-    k_adjoint<8><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+    if (array->n_samples % 2 == 0)
+        k_adjoint<true><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+    else
+        k_adjoint<false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
     return last_status();
 }

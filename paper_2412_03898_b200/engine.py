@@ -51,6 +51,28 @@ def scheduled_lr(lr0, iteration, step_size, drop_rate):
     return lr0 * drop_rate ** (iteration // step_size)
 
 
+def morton_order(mu: np.ndarray, bits: int = 10) -> np.ndarray:
+    """Stable Z-order of ball centres (the engine's internal ball layout).
+
+    Spatially close balls share 32-ball culling groups in the forward and
+    read overlapping residual windows in the adjoint (L1 reuse).  The
+    reference's own initial clouds are lattices (geometry.py:129-133), i.e.
+    already ordered; this makes any input order behave the same.
+    """
+    mu = np.asarray(mu, dtype=np.float64).reshape(-1, 3)
+    if len(mu) == 0:
+        return np.zeros(0, dtype=np.int64)
+    lo = mu.min(axis=0)
+    span = np.maximum(mu.max(axis=0) - lo, 1e-12)
+    q = np.minimum(((mu - lo) / span * (1 << bits)).astype(np.int64),
+                   (1 << bits) - 1)
+    code = np.zeros(len(mu), dtype=np.int64)
+    for bit in range(bits):
+        for ax in range(3):
+            code |= ((q[:, ax] >> bit) & 1) << (3 * bit + ax)
+    return np.argsort(code, kind="stable").astype(np.int64)
+
+
 def select_frames(n_frames: int, batch: int, rng) -> np.ndarray:
     """reconstruction.py:246-250 (same RNG draws as the reference)."""
     if batch <= 0 or batch >= n_frames:
@@ -96,7 +118,7 @@ class IterationEngine:
 
     def __init__(self, cloud, array, observed, frame_times, config, *,
                  shard=None, process_group=None, use_graph=True,
-                 device=None):
+                 device=None, spatial_order=True):
         _lib.load_library()
         self.cfg = config
         self.basis = getattr(cloud, "basis", getattr(config, "basis",
@@ -144,10 +166,18 @@ class IterationEngine:
                               device=self.device)
         self.params = self.layout.views(self.P)
         self.grads = self.layout.views(self.Gf)
+        # internal ball order (identity or Morton); outputs are un-permuted
+        mu_host = cloud.mu.detach().cpu().numpy() if isinstance(
+            cloud.mu, torch.Tensor) else np.asarray(cloud.mu)
+        self.order = morton_order(mu_host) if spatial_order else \
+            np.arange(B, dtype=np.int64)
+        self.inverse = np.empty_like(self.order)
+        self.inverse[self.order] = np.arange(B, dtype=np.int64)
+        order_dev = torch.as_tensor(self.order, device=self.device)
         for name in self.params:
-            src = getattr(cloud, name)
-            self.params[name].copy_(to_device(src, torch.float64)
-                                    .reshape(self.params[name].shape))
+            src = to_device(getattr(cloud, name), torch.float64)
+            self.params[name].copy_(src.reshape(self.params[name].shape)
+                                    .index_select(0, order_dev))
         self.step_count = {s.name: 0 for s in self.layout.segments}
         p = self.params
         self.dcloud = DeviceCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
@@ -339,7 +369,10 @@ class IterationEngine:
         self.allreduce()
         loss, flags, coinc = self.check_and_status()
         if coinc != _lib.INT64_MAX:
-            raise_if_coincident(coinc, self.mu_t, self.darr.positions)
+            b, m = divmod(coinc, self.darr.M)
+            raise_if_coincident(int(self.order[b]) * self.darr.M + m,
+                                self.mu_t[0][torch.as_tensor(self.inverse, device=self.device)],
+                                self.darr.positions)
         if not math.isfinite(loss):
             raise RuntimeError(f"non-finite loss at iteration {iteration}")
         if flags.any():
@@ -360,12 +393,15 @@ class IterationEngine:
 
     # ------------------------------------------------------------ views
     def cloud(self) -> DynamicCloud:
-        p = {k: v.cpu().numpy().copy() for k, v in self.params.items()}
+        p = {k: v.cpu().numpy()[self.inverse].copy()
+             for k, v in self.params.items()}
         return DynamicCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
                             p.get("sigma"), p["omega"], basis=self.basis)
 
     def grads_numpy(self) -> dict:
-        return {k: v.double().cpu().numpy() for k, v in self.grads.items()}
+        """Parameter gradients in the caller's ball order (float64)."""
+        return {k: v.double().cpu().numpy()[self.inverse]
+                for k, v in self.grads.items()}
 
 
 def identity_cloud(p0, a0, mu, n_basis: int, basis: str = "gauss"):

