@@ -160,55 +160,57 @@ struct FwdArgs {
 };
 
 // Record of one (ball, sensor) pair, written by its setup lane:
-//   r0 = {je0, niter | near << 30, X0, c}   X0 = s (R - v t_je0), or X at jr (exact)
-//   r1 = {vs, Y0, span = je1 - je0, jr}
-// niter = 0 marks an empty pair.
+//   r0 = {je0 | je1 << 15 | near << 30, X0, c, vs}  (je1 == je0: empty pair)
+//   r1 = {X at jr, Y at jr, jr, -}                 (exact / near-field only)
+// X0 = s (R - v t_je0).  The trip count is ball-uniform (from a0), so the two
+// half-warps never need to agree on it.
 
 // Both half-warps sweep the same ball for their own sensor: lane `sub` of a
 // half owns sample pairs (j, j+1), j = je0 + 2 sub + FSTR n, so each half's
 // float2 access is 128 contiguous bytes of its own trace (one conflict-free
-// wavefront).  Trip counts of the two halves differ by at most one; the loop
-// runs the larger with per-lane predication.
-template <bool EXACT>
-__device__ __forceinline__ void fwd_sweep2(float* __restrict__ tr, float4 r0, float4 r1,
-                                           float2 sub2, int sub) {
-    const int je0 = __float_as_int(r0.x);
-    const int wn = __float_as_int(r0.y);
-    const int nl = wn & 0x3fffffff;
-    const bool near = (wn >> 30) & 1;
-    const int nmax = max(nl, __shfl_xor_sync(0xffffffffu, nl, FL));
-    if (nmax == 0) return;
-    const int span = __float_as_int(r1.z) - 2 * sub;
-    const float2 cc = splat2(r0.w);
-    const float vs = r1.x;
+// wavefront).
+__device__ __forceinline__ void fwd_sweep_fast(float* __restrict__ tr, float4 r0, int niter,
+                                               float2 sub2, int sub) {
+    const int w = __float_as_int(r0.x);
+    const int je0 = w & 0x7fff;
+    // pair-iterations this lane owns (its last sample pair starts before je1)
+    const int nl = (((w >> 15) & 0x7fff) - je0 - 2 * sub + FSTR - 1) / FSTR;
+    const float2 cc = splat2(r0.z);
+    float2 x = ffma2(sub2, splat2(-r0.w), splat2(r0.y));
+    const float2 dx = splat2(-(float)FSTR * r0.w);
     float2* p = reinterpret_cast<float2*>(tr + je0) + sub;
-    const bool anynear = __any_sync(0xffffffffu, near && nl > 0);
-    if (!EXACT && !anynear) {
-        float2 x = ffma2(sub2, splat2(-vs), splat2(r0.z));
-        const float2 dx = splat2(-(float)FSTR * vs);
-#pragma unroll 4
-        for (int n = 0; n < nmax; ++n, p += FL) {
+    for (int n = 0; n < niter; n += 4, p += 4 * FL) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
             const float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
-            if (FSTR * n < span) *p = ffma2(cc, v, *p);
+            if (n + u < nl) p[u * FL] = ffma2(cc, v, p[u * FL]);
             x = fadd2(x, dx);
         }
-    } else {
-        // exact / near field: x (and y) from the exact integer offset to the
-        // reference sample (r1.w) every iteration; r0.z / r1.y are X / Y there
-        const int jr = __float_as_int(r1.w);
-        const float Xr = EXACT ? r0.z : fmaf((float)(je0 - jr), vs, r0.z);   // X at jr
-        const float Yr = r1.y;                                               // Y at jr
-        float2 k = fadd2(sub2, splat2((float)(je0 - jr)));
-        for (int n = 0; n < nmax; ++n, p += FL) {
-            const float2 x = ffma2(k, splat2(-vs), splat2(Xr));
-            float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
-            if (near) {
-                const float2 y = ffma2(k, splat2(vs), splat2(Yr));
-                v = ffma2(y, ex2n_2(fmul2(y, y)), v);
-            }
-            if (FSTR * n < span) *p = ffma2(cc, v, *p);
-            k = fadd2(k, splat2((float)FSTR));
+    }
+}
+
+// Exact window / near field: x (and y) from the exact integer offset to the
+// wavefront sample jr every iteration (the window may start far from it).
+__device__ __forceinline__ void fwd_sweep_slow(float* __restrict__ tr, float4 r0, float4 r1,
+                                               int niter, float2 sub2, int sub) {
+    const int w = __float_as_int(r0.x);
+    const int je0 = w & 0x7fff;
+    const int span = ((w >> 15) & 0x7fff) - je0 - 2 * sub;
+    const bool near = (w >> 30) & 1;
+    const float vs = r0.w;
+    const float2 cc = splat2(r0.z);
+    const int jr = __float_as_int(r1.z);
+    float2 k = fadd2(sub2, splat2((float)(je0 - jr)));
+    float2* p = reinterpret_cast<float2*>(tr + je0) + sub;
+    for (int n = 0; n < niter; ++n, p += FL) {
+        const float2 x = ffma2(k, splat2(-vs), splat2(r1.x));
+        float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
+        if (near) {
+            const float2 y = ffma2(k, splat2(vs), splat2(r1.y));
+            v = ffma2(y, ex2n_2(fmul2(y, y)), v);
         }
+        if (FSTR * n < span) *p = ffma2(cc, v, *p);
+        k = fadd2(k, splat2((float)FSTR));
     }
 }
 
@@ -316,6 +318,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 pass = EXACT || r < 1e-3f || (r + w >= d_lo && r - w <= d_hi);
             }
             float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+            bool slow = false;
             if (pass) {
                 const float av = cur.w;
                 const float s = scale_of(av);
@@ -332,24 +335,39 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     const float c = __fdividef(0.5f * __ldg(a.p0 + fb + i), (float)q.R * s);
                     const float vs = vdt * s;
                     const int je0 = q.jl & ~1;
-                    const int span = ((q.jh + 1) & ~1) - je0;
-                    const int niter = (span + FSTR - 1) / FSTR;
-                    const float X0 = EXACT ? q.X : fmaf((float)(q.jr - je0), vs, q.X);
-                    q0 = make_float4(__int_as_float(je0),
-                                     __int_as_float(niter | (q.near ? 1 << 30 : 0)), X0, c);
-                    q1 = make_float4(vs, q.Y, __int_as_float(span), __int_as_float(q.jr));
+                    const int je1 = (q.jh + 1) & ~1;
+                    const float X0 = fmaf((float)(q.jr - je0), vs, q.X);
+                    q0 = make_float4(__int_as_float(je0 | (je1 << 15) | (q.near ? 1 << 30 : 0)),
+                                     X0, c, vs);
+                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), 0.f);
+                    slow = EXACT || q.near;
                 }
             }
             ws.rec[lane][0] = q0;
             ws.rec[lane][1] = q1;
             const unsigned pm = __ballot_sync(0xffffffffu, pass);
+            const bool anyslow = __any_sync(0xffffffffu, slow);
             unsigned mask = (pm | (pm >> FL)) & ((1u << FL) - 1u);   // balls with any pair
             __syncwarp();
             while (mask) {
                 const int b = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const int src = h * FL + b;
-                fwd_sweep2<EXACT>(tr, ws.rec[src][0], ws.rec[src][1], sub2, sub);
+                // ball-uniform trip count: window <= 2 support a0 / (v dt) + 4
+                const float ab = __shfl_sync(0xffffffffu, cur.w, b);
+                const int niter =
+                    EXACT ? (s1 - s0 + FSTR + 1) / FSTR
+                          : (int)(ab * (2.f * sup / vdt) + 4.f + (float)(FSTR - 1)) / FSTR;
+                const float4 r0 = ws.rec[src][0];
+                if (!anyslow) {
+                    fwd_sweep_fast(tr, r0, niter, sub2, sub);
+                } else {
+                    const bool sl = EXACT || ((__float_as_int(r0.x) >> 30) & 1);
+                    if (__any_sync(0xffffffffu, sl))
+                        fwd_sweep_slow(tr, r0, ws.rec[src][1], niter, sub2, sub);
+                    else
+                        fwd_sweep_fast(tr, r0, niter, sub2, sub);
+                }
                 __syncwarp();
             }
         }
@@ -566,32 +584,26 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
                     recur_init(x, D, e, g);
                     int n = (je1 - j + LSTRIDE - 1) / LSTRIDE;   // sample pairs of this lane
                     if (ALIGNED) {
-                        // software-pipelined: the next 4 sample pairs are in
-                        // flight while the current 4 are accumulated
+                        // full chunks of 4 sample pairs: 4 independent loads in
+                        // flight, then 4 accumulation steps; then the remainder
                         const float2* p = reinterpret_cast<const float2*>(row + j);
-                        float2 nx[4];
+                        for (; n >= 4; n -= 4, p += 4 * LG) {
+                            float2 rr[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            nx[u] = u < n ? __ldg(p + u * LG) : splat2(0.f);
-                        while (n > 0) {
-                            float2 cr[4];
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) cr[u] = nx[u];
-                            const int nc = n;
-                            p += 4 * LG;
-                            n -= 4;
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                nx[u] = u < n ? __ldg(p + u * LG) : splat2(0.f);
+                            for (int u = 0; u < 4; ++u) rr[u] = __ldg(p + u * LG);
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                if (u < nc) {
-                                    accum_pair(cr[u], e, x, A0, A1, A2, A3);
-                                    e = fmul2(e, g);
-                                    g = fmul2(g, h2);
-                                    x = fadd2(x, mD2);
-                                }
+                                accum_pair(rr[u], e, x, A0, A1, A2, A3);
+                                e = fmul2(e, g);
+                                g = fmul2(g, h2);
+                                x = fadd2(x, mD2);
                             }
+                        }
+                        for (; n > 0; --n, p += LG) {
+                            accum_pair(__ldg(p), e, x, A0, A1, A2, A3);
+                            e = fmul2(e, g);
+                            g = fmul2(g, h2);
+                            x = fadd2(x, mD2);
                         }
                     } else {
                         for (; j < je1; j += LSTRIDE) {
