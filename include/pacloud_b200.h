@@ -211,6 +211,24 @@ int pc_compact_index(const uint8_t *keep, const uint8_t *append,
                      void *workspace, size_t workspace_bytes,
                      pc_stream_t stream);
 
+/* Config-5 densify masks (builder-defined rule; the
+ * reference has pruning only, reconstruction.py:217-226):
+ *   keep[b]  = !(p0[b] < p0_min)
+ *   split[b] = keep[b] && |g[b]| > threshold       (g = dL/dp0, f32)
+ * `threshold` is the numpy 'linear' percentile of |g| (computed by the host
+ * from device order statistics).  counts (device int64[2]) receive
+ * (#keep, #split). */
+int pc_densify_masks(const double *p0, const float *g, int64_t n_balls,
+                     double p0_min, double threshold, uint8_t *keep,
+                     uint8_t *split, int64_t *counts, pc_stream_t stream);
+
+/* After the gather of a densify step (new order = survivors then children):
+ * p0[i] *= 0.5 where halve[i] (split parents and their children) and
+ * mu[i,0] += shift * a0[i] where child[i]. */
+int pc_densify_apply(double *p0, double *mu, const double *a0,
+                     const uint8_t *halve, const uint8_t *child,
+                     int64_t n_balls, double shift, pc_stream_t stream);
+
 /* dst[i, :] = src[index[i], :] for i < n_rows (row_bytes a multiple of 4). */
 int pc_gather_rows(const void *src, void *dst, const int64_t *index,
                    int64_t n_rows, int64_t row_bytes, pc_stream_t stream);

@@ -81,6 +81,10 @@ SIGNATURES = {
                                 _P]),
     "pc_compact_index": (c_int32, [_P, _P, c_int64, _P, _P, _P, c_size_t,
                                    _P]),
+    "pc_densify_masks": (c_int32, [_P, _P, c_int64, c_double, c_double, _P,
+                                   _P, _P, _P]),
+    "pc_densify_apply": (c_int32, [_P, _P, _P, _P, _P, c_int64, c_double,
+                                   _P]),
     "pc_gather_rows": (c_int32, [_P, _P, _P, c_int64, c_int64, _P]),
     "pc_version": (c_char_p, []),
 }

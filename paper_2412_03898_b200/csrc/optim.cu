@@ -252,9 +252,88 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ src
     }
 }
 
+__global__ void __launch_bounds__(256) k_densify_masks(const double* __restrict__ p0,
+                                                       const float* __restrict__ g, int64_t n,
+                                                       double p0_min, double thr,
+                                                       uint8_t* __restrict__ keep,
+                                                       uint8_t* __restrict__ split,
+                                                       unsigned long long* __restrict__ counts) {
+    (void)counts;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t k = (p0[i] < p0_min) ? 0 : 1;
+        const uint8_t s = (k && fabs((double)g[i]) > thr) ? 1 : 0;
+        keep[i] = k;
+        split[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_count_u8(const uint8_t* __restrict__ a,
+                                                  const uint8_t* __restrict__ b, int64_t n,
+                                                  unsigned long long* __restrict__ counts) {
+    unsigned long long ca = 0, cb = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        ca += a[i];
+        cb += b[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ca += __shfl_xor_sync(0xffffffffu, ca, o);
+        cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(counts, ca);
+        atomicAdd(counts + 1, cb);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_densify_apply(double* __restrict__ p0,
+                                                       double* __restrict__ mu,
+                                                       const double* __restrict__ a0,
+                                                       const uint8_t* __restrict__ halve,
+                                                       const uint8_t* __restrict__ child,
+                                                       int64_t n, double shift) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (halve[i]) p0[i] = 0.5 * p0[i];
+        if (child[i]) mu[3 * i] = mu[3 * i] + shift * a0[i];
+    }
+}
+
 }  // namespace pc
 
 using namespace pc;
+
+extern "C" int pc_densify_masks(const double* p0, const float* g, int64_t n_balls, double p0_min,
+                                double threshold, uint8_t* keep, uint8_t* split, int64_t* counts,
+                                pc_stream_t stream) {
+    if (n_balls < 0 || !counts) return PC_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), st) != cudaSuccess) return PC_ERR_CUDA;
+    if (n_balls == 0) return PC_OK;
+    if (!p0 || !g || !keep || !split) return PC_ERR_ARGUMENT;
+    int64_t blocks = (n_balls + 255) / 256;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    k_densify_masks<<<(unsigned)blocks, 256, 0, st>>>(p0, g, n_balls, p0_min, threshold, keep,
+                                                      split, nullptr);
+    k_count_u8<<<(unsigned)blocks, 256, 0, st>>>(keep, split, n_balls,
+                                                 reinterpret_cast<unsigned long long*>(counts));
+    return last_status();
+}
+
+extern "C" int pc_densify_apply(double* p0, double* mu, const double* a0, const uint8_t* halve,
+                                const uint8_t* child, int64_t n_balls, double shift,
+                                pc_stream_t stream) {
+    if (n_balls < 0) return PC_ERR_ARGUMENT;
+    if (n_balls == 0) return PC_OK;
+    if (!p0 || !mu || !a0 || !halve || !child) return PC_ERR_ARGUMENT;
+    int64_t blocks = (n_balls + 255) / 256;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    k_densify_apply<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(p0, mu, a0, halve, child,
+                                                                     n_balls, shift);
+    return last_status();
+}
 
 extern "C" int pc_l2_loss(const double* predicted, const double* observed, int64_t n, double* out,
                           pc_stream_t stream) {

@@ -195,7 +195,7 @@ class IterationEngine:
 
     # ------------------------------------------------------------ buffers
     def _ensure_buffers(self, F: int):
-        if self._bufs_F == F:
+        if self._bufs_F == F and self.mu_t.shape[1] == self.B:
             return
         dev, B, M, T = self.device, self.B, self.darr.M, self.darr.T
         self.t_dev = torch.zeros(F, dtype=torch.float64, device=dev)
@@ -390,6 +390,111 @@ class IterationEngine:
                 done += names
         self.apply_update(lrs)
         return loss
+
+    # ------------------------------------------------------------ densify
+    def p0_grad_threshold(self, q: float = 90.0) -> float:
+        """numpy.percentile(|dL/dp0|, q, method='linear') of the last
+        computed gradient: device sort (order statistics), then numpy's own
+        index / lerp arithmetic (numpy/lib/_function_base_impl.py _lerp) on
+        the two neighbours, in float64 on the host."""
+        g = self.grads["p0"].abs().double()
+        n = int(g.numel())
+        if n == 0:
+            return 0.0
+        srt = torch.sort(g).values
+        qq = float(np.float64(q) / np.float64(100.0))
+        virtual = (n - 1) * qq
+        if virtual >= n - 1:
+            return float(srt[-1].item())
+        if virtual < 0:
+            return float(srt[0].item())
+        prev = math.floor(virtual)
+        gamma = virtual - prev
+        ab = srt[prev:prev + 2].cpu().numpy()
+        a, b = float(ab[0]), float(ab[1])
+        diff = b - a
+        return b - diff * (1.0 - gamma) if gamma >= 0.5 else a + diff * gamma
+
+    def densify(self, p0_min: float = 0.01, q: float = 90.0,
+                child_shift: float = 0.5, max_balls: int | None = None):
+        """Config-5 adaptive step (builder-defined): prune
+        p0 < p0_min, split balls with |dL/dp0| above its q-th percentile.
+        New order = survivors in order, then one child per split survivor in
+        parent order (pc_compact_index); every parameter and Adam moment is
+        gathered (pc_gather_rows, step counts preserved as in
+        reconstruction.py:95-100); split parents and children get half the
+        pressure and children move +child_shift*a0 along x
+        (pc_densify_apply); children start with zero moments.
+        Returns (n_pruned, n_children)."""
+        lib = _lib.load_library()
+        B = self.B
+        dev = self.device
+        thr = self.p0_grad_threshold(q)
+        keep = torch.empty(B, dtype=torch.uint8, device=dev)
+        split = torch.empty(B, dtype=torch.uint8, device=dev)
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        _lib.check(lib.pc_densify_masks(
+            _lib.ptr(self.params["p0"]), _lib.ptr(self.grads["p0"]), B,
+            float(p0_min), float(thr), _lib.ptr(keep), _lib.ptr(split),
+            _lib.ptr(counts), _lib.stream()), "pc_densify_masks")
+        n_keep, n_split = (int(v) for v in counts.cpu().tolist())
+        if n_keep == 0:
+            raise RuntimeError("all balls pruned; lower the densify p0_min")
+        if max_balls is not None and n_keep + n_split > max_balls:
+            allowed = max(0, int(max_balls) - n_keep)
+            split = (split.bool() & (torch.cumsum(split.to(torch.int64), 0)
+                                     <= allowed)).to(torch.uint8)
+            n_split = allowed if allowed < n_split else n_split
+        ws = torch.empty(int(lib.pc_compact_workspace_bytes(B)),
+                         dtype=torch.uint8, device=dev)
+        index = torch.empty(2 * B, dtype=torch.int64, device=dev)
+        n_out = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.check(lib.pc_compact_index(
+            _lib.ptr(keep), _lib.ptr(split), B, _lib.ptr(index),
+            _lib.ptr(n_out), _lib.ptr(ws), ws.numel(), _lib.stream()),
+            "pc_compact_index")
+        B2 = n_keep + n_split
+        index = index[:B2]
+        per_channel = self.basis == "gauss" and self.params["theta"].dim() == 3
+        layout = ParamLayout(B2, self.N, self.basis, per_channel)
+        f64 = dict(dtype=torch.float64, device=dev)
+        P2 = torch.empty(layout.total, **f64)
+        M2 = torch.empty(layout.total, **f64)
+        V2 = torch.empty(layout.total, **f64)
+        for old, new in zip(self.layout.segments, layout.segments):
+            row = (old.size // B) * 8
+            for src, dst in ((self.P, P2), (self.Mo, M2), (self.Vo, V2)):
+                _lib.check(lib.pc_gather_rows(
+                    _lib.ptr(src[old.offset:]), _lib.ptr(dst[new.offset:]),
+                    _lib.ptr(index), B2, row, _lib.stream()),
+                    "pc_gather_rows")
+            if n_split:
+                M2[new.offset + (new.size // B2) * n_keep:
+                   new.offset + new.size].zero_()
+                V2[new.offset + (new.size // B2) * n_keep:
+                   new.offset + new.size].zero_()
+        halve = torch.index_select(split, 0, index)
+        child = torch.zeros(B2, dtype=torch.uint8, device=dev)
+        child[n_keep:] = 1
+        pv = layout.views(P2)
+        _lib.check(lib.pc_densify_apply(
+            _lib.ptr(pv["p0"]), _lib.ptr(pv["mu"]), _lib.ptr(pv["a0"]),
+            _lib.ptr(halve), _lib.ptr(child), B2, float(child_shift),
+            _lib.stream()), "pc_densify_apply")
+        # swap in the new cloud (internal order becomes the caller's order)
+        self.layout, self.B = layout, B2
+        self.P, self.Mo, self.Vo = P2, M2, V2
+        self.Gf = torch.zeros(layout.total, dtype=torch.float32, device=dev)
+        self.params = layout.views(self.P)
+        self.grads = layout.views(self.Gf)
+        p = self.params
+        self.dcloud = DeviceCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
+                                  p.get("sigma"), p["omega"], self.basis)
+        self.order = np.arange(B2, dtype=np.int64)
+        self.inverse = self.order.copy()
+        self._bufs_F = -1
+        self._graph = None
+        return B - n_keep, n_split
 
     # ------------------------------------------------------------ views
     def cloud(self) -> DynamicCloud:

@@ -428,3 +428,71 @@ def test_engine_minibatch_frames_and_steps(pc):
         # the Adam updates themselves (sign-like steps) agree closely
         assert rel_l2(getattr(got, k) - init,
                       getattr(ref_cloud, k) - init) < 1e-2, k
+
+
+# ------------------------------------------------------------ config-5 densify
+
+def _engine_small(pc, B=3000, seed=4, spatial=False):
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.engine import IterationEngine
+    prob = synth.make_problem(5, seed=seed, n_balls=B, n_sensors=32,
+                              n_frames=3)
+    obs = np.zeros((prob.n_frames, 32, prob.array.n_samples), np.float32)
+    eng = IterationEngine(prob.cloud, prob.array, obs, prob.frame_times,
+                          prob.config, spatial_order=spatial)
+    return prob, eng
+
+
+@pytest.mark.parametrize("B", [1000, 3000, 4097])
+def test_densify_threshold_is_numpy_percentile(pc, B):
+    import torch
+    _, eng = _engine_small(pc, B)
+    rng = np.random.default_rng(B)
+    g = rng.normal(size=B).astype(np.float32)
+    eng.grads["p0"].copy_(torch.as_tensor(g))
+    want = float(np.percentile(np.abs(g.astype(np.float64)), 90))
+    assert eng.p0_grad_threshold(90.0) == want
+
+
+def test_densify_masks_order_and_params_bit_exact(pc):
+    import torch
+    prob, eng = _engine_small(pc, 2000)
+    rng = np.random.default_rng(9)
+    B = eng.B
+    p0 = rng.uniform(0.0, 0.05, B)
+    g = rng.normal(size=B).astype(np.float32)
+    eng.params["p0"].copy_(torch.as_tensor(p0))
+    eng.grads["p0"].copy_(torch.as_tensor(g))
+    before = {k: v.cpu().numpy().copy() for k, v in eng.params.items()}
+    n_pruned, n_children = eng.densify(p0_min=0.01, q=90.0, child_shift=0.5)
+    keep, split, index, is_child = oracle.densify_plan(
+        p0, g.astype(np.float64), p0_min=0.01, q=90.0)
+    assert n_pruned == int((~keep).sum()) and n_children == int(split.sum())
+    want = oracle.apply_densify(before, index, is_child, split, keep,
+                                child_shift=0.5)
+    got = eng.cloud()
+    for k in ("p0", "a0", "mu", "omega"):
+        assert np.array_equal(getattr(got, k), want[k]), k
+    # children start with zero Adam moments
+    seg = eng.layout.by_name["omega"]
+    m = eng.Mo[seg.offset:seg.offset + seg.size].view(seg.shape)
+    assert bool((m[int(keep.sum()):] == 0).all())
+
+
+def test_growth_loop_runs_and_grows(pc):
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.engine import IterationEngine
+    prob = synth.make_problem(5, seed=5, n_balls=800, n_sensors=48,
+                              n_frames=4)
+    obs = np.stack([oracle.forward_frame(oracle.States(a, p, m), prob.array)
+                    for a, p, m in prob.gt_frames]).astype(np.float32)
+    eng = IterationEngine(prob.cloud, prob.array, obs, prob.frame_times,
+                          prob.config, spatial_order=False)
+    sizes = [eng.B]
+    for it in range(6):
+        loss = eng.iterate(it, np.arange(prob.n_frames))
+        assert np.isfinite(loss)
+        if it % 2 == 1:
+            eng.densify(p0_min=0.01, q=90.0, max_balls=1200)
+            sizes.append(eng.B)
+    assert sizes[-1] > sizes[0] and sizes[-1] <= 1200
