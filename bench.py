@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sensors", type=int, default=0)
+    ap.add_argument("--densify-every", type=int, default=8,
+                    help="config 5: densify/prune every N iterations")
+    ap.add_argument("--max-balls", type=int, default=500000,
+                    help="config 5: growth cap")
     return ap.parse_args()
 
 
@@ -267,7 +271,8 @@ def run_ours(args, rank, world, local):
     else:
         local_frames = frame_shard(frames_all, rank, world)
         eng = IterationEngine(prob.cloud, arr, obs, prob.frame_times, cfg,
-                              shard="frames")
+                              shard="frames",
+                              spatial_order=args.config != 5)
     del obs
     torch.cuda.synchronize()
 
@@ -278,8 +283,14 @@ def run_ours(args, rank, world, local):
         if world > 1:
             torch.distributed.barrier()
 
-    for _ in range(args.warmup):
+    def step(it):
+        """One iteration (+ the config-5 densify/prune when due)."""
         eng.iterate(it, frames_all)
+        if args.config == 5 and (it + 1) % args.densify_every == 0:
+            eng.densify(p0_min=0.01, q=90.0, max_balls=args.max_balls)
+
+    for _ in range(args.warmup):
+        step(it)
         it += 1
     torch.cuda.synchronize()
 
@@ -288,11 +299,13 @@ def run_ours(args, rank, world, local):
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
+    pairs_done = 0
     with ClockSampler(local) as clocks:
         for k in range(args.steps):
             flush.zero_()
+            pairs_done += eng.B * M * F
             ev[k][0].record()
-            eng.iterate(it, frames_all)
+            step(it)
             ev[k][1].record()
             it += 1
         torch.cuda.synchronize()
@@ -303,12 +316,13 @@ def run_ours(args, rank, world, local):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    pairs = B * M * F
+    pairs = pairs_done / args.steps            # per step (B grows in config 5)
     value = pairs / (ms * 1e-3)
 
     # ---- dominant kernels: fwd + adj, timed live with events on the
     # launching stream (eager, same buffers), and exact algorithmic work
     F_loc = len(local_frames)
+    eng._ensure_buffers(F_loc)          # B may have changed (config-5 densify)
     eng.t_dev.copy_(torch.as_tensor(prob.frame_times[local_frames]))
     from paper_2412_03898_b200.deformation import deform_states_device
     from paper_2412_03898_b200.radiator import state_grads_device
@@ -333,6 +347,7 @@ def run_ours(args, rank, world, local):
         if r:
             t_fwd += e[0].elapsed_time(e[1]) / reps
             t_adj += e[1].elapsed_time(e[2]) / reps
+    B = eng.B
     S = support_samples_torch(eng.mu_t, eng.a0_t, eng.darr.positions,
                               eng.darr.v, eng.darr.t0, eng.darr.dt,
                               eng.darr.T, cfg.support_sigmas)
@@ -376,6 +391,8 @@ def run_ours(args, rank, world, local):
             ee[k][0].record()
             eng.observed.copy_(host_obs, non_blocking=True)
             losses.append(eng.iterate(it, frames_all))   # D2H of the loss
+            if args.config == 5 and (it + 1) % args.densify_every == 0:
+                eng.densify(p0_min=0.01, q=90.0, max_balls=args.max_balls)
             ee[k][1].record()
             it += 1
         torch.cuda.synchronize()
@@ -384,7 +401,7 @@ def run_ours(args, rank, world, local):
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": pairs / (ems * 1e-3), "unit": UNIT,
+        e2e = {"value": eng.B * M * F / (ems * 1e-3), "unit": UNIT,
                "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": 8 + 4 * len(eng.layout.segments) + 8,
                "api": "IterationEngine.iterate with observed copied from "
@@ -415,6 +432,7 @@ def run_ours(args, rank, world, local):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
             "final_loss": float(eng.loss_total.item()),
+            "final_balls": int(eng.B),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
