@@ -49,8 +49,9 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     p.Tseg = T < FWD_TSEG_MAX ? ((T + 31) / 32) * 32 : FWD_TSEG_MAX;
     p.nseg = (T + p.Tseg - 1) / p.Tseg;
     const int64_t tiles = (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW);
-    const int64_t base = tiles * F;          // CTAs with work (about one segment each)
-    const int64_t want = 6LL * num_sms();
+    // CTAs with work: the active arrival range typically spans half of T
+    const int64_t base = tiles * F * (p.nseg > 1 ? p.nseg / 2 : 1);
+    const int64_t want = 4LL * num_sms();
     int64_t c = base >= want ? 1 : (want + base - 1) / base;
     const int64_t cmax = B / 256 > 1 ? B / 256 : 1;
     if (c > cmax) c = cmax;
