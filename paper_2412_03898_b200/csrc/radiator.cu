@@ -49,9 +49,10 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     p.Tseg = T < FWD_TSEG_MAX ? ((T + 31) / 32) * 32 : FWD_TSEG_MAX;
     p.nseg = (T + p.Tseg - 1) / p.Tseg;
     const int64_t tiles = (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW);
-    // CTAs with work: the active arrival range typically spans half of T
+    // CTAs with work (the active arrival range typically spans half of T);
+    // ask for >= 2 waves of resident CTAs (6 per SM) so the tail stays short
     const int64_t base = tiles * F * (p.nseg > 1 ? p.nseg / 2 : 1);
-    const int64_t want = 4LL * num_sms();
+    const int64_t want = 12LL * num_sms();
     int64_t c = base >= want ? 1 : (want + base - 1) / base;
     const int64_t cmax = B / 256 > 1 ? B / 256 : 1;
     if (c > cmax) c = cmax;
@@ -170,34 +171,57 @@ struct FwdArgs {
 // half owns sample pairs (j, j+1), j = je0 + 2 sub + FSTR n, so each half's
 // float2 access is 128 contiguous bytes of its own trace (one conflict-free
 // wavefront).
-__device__ __forceinline__ void fwd_sweep_fast(float* __restrict__ tr, float4 r0, int niter,
-                                               float2 sub2, int sub) {
+// One fast-path step: the sample pair at p (if the lane's window covers it),
+// then x advances one lane stride.
+__device__ __forceinline__ void fwd_step(float2* __restrict__ p, bool live, float2& x, float2 dx,
+                                         float2 cc) {
+    const float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
+    if (live) *p = ffma2(cc, v, *p);
+    x = fadd2(x, dx);
+}
+
+// Fast path.  Record r0 = {je0 | niter << 15, X0, c, vs} with niter the
+// larger trip count of the two half-warps (set up by the setup pass), and
+// r1.w = je1 - je0.  Each lane writes only inside its own window; unrolled by
+// 4, predicates compare the lane's remaining sample count with constants.
+__device__ __forceinline__ void fwd_sweep_fast(float* __restrict__ tr, float4 r0, int span,
+                                               float2 sub2, int sub2i) {
     const int w = __float_as_int(r0.x);
     const int je0 = w & 0x7fff;
-    // pair-iterations this lane owns (its last sample pair starts before je1)
-    const int nl = (((w >> 15) & 0x7fff) - je0 - 2 * sub + FSTR - 1) / FSTR;
+    const int niter = (w >> 15) & 0x7fff;
+    int rem = span - sub2i;                              // samples left from this lane's start
+    const float vs = r0.w;
     const float2 cc = splat2(r0.z);
-    float2 x = ffma2(sub2, splat2(-r0.w), splat2(r0.y));
-    const float2 dx = splat2(-(float)FSTR * r0.w);
-    float2* p = reinterpret_cast<float2*>(tr + je0) + sub;
-    for (int n = 0; n < niter; n += 4, p += 4 * FL) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
-            if (n + u < nl) p[u * FL] = ffma2(cc, v, p[u * FL]);
-            x = fadd2(x, dx);
-        }
+    float2 x = ffma2(sub2, splat2(-vs), splat2(r0.y));
+    const float2 dx = splat2(-(float)FSTR * vs);
+    float2* p = reinterpret_cast<float2*>(tr + je0 + sub2i);
+    int n = niter;
+    for (; n >= 4; n -= 4, p += 4 * FL, rem -= 4 * FSTR) {
+        fwd_step(p, rem > 0, x, dx, cc);
+        fwd_step(p + FL, rem > FSTR, x, dx, cc);
+        fwd_step(p + 2 * FL, rem > 2 * FSTR, x, dx, cc);
+        fwd_step(p + 3 * FL, rem > 3 * FSTR, x, dx, cc);
     }
+    if (n >= 2) {
+        fwd_step(p, rem > 0, x, dx, cc);
+        fwd_step(p + FL, rem > FSTR, x, dx, cc);
+        p += 2 * FL;
+        rem -= 2 * FSTR;
+        n -= 2;
+    }
+    if (n) fwd_step(p, rem > 0, x, dx, cc);
 }
 
 // Exact window / near field: x (and y) from the exact integer offset to the
 // wavefront sample jr every iteration (the window may start far from it).
 __device__ __forceinline__ void fwd_sweep_slow(float* __restrict__ tr, float4 r0, float4 r1,
-                                               int niter, float2 sub2, int sub) {
+                                               float2 sub2, int sub) {
     const int w = __float_as_int(r0.x);
     const int je0 = w & 0x7fff;
-    const int span = ((w >> 15) & 0x7fff) - je0 - 2 * sub;
     const bool near = (w >> 30) & 1;
+    const int wl = __float_as_int(r1.w);               // je1 - je0 (0: empty pair)
+    const int nl = (wl - 2 * sub + FSTR - 1) / FSTR;
+    const int niter = max(nl, __shfl_xor_sync(0xffffffffu, nl, FL));
     const float vs = r0.w;
     const float2 cc = splat2(r0.z);
     const int jr = __float_as_int(r1.z);
@@ -210,7 +234,7 @@ __device__ __forceinline__ void fwd_sweep_slow(float* __restrict__ tr, float4 r0
             const float2 y = ffma2(k, splat2(vs), splat2(r1.y));
             v = ffma2(y, ex2n_2(fmul2(y, y)), v);
         }
-        if (FSTR * n < span) *p = ffma2(cc, v, *p);
+        if (n < nl) *p = ffma2(cc, v, *p);
         k = fadd2(k, splat2((float)FSTR));
     }
 }
@@ -338,11 +362,17 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     const int je0 = q.jl & ~1;
                     const int je1 = (q.jh + 1) & ~1;
                     const float X0 = fmaf((float)(q.jr - je0), vs, q.X);
-                    q0 = make_float4(__int_as_float(je0 | (je1 << 15) | (q.near ? 1 << 30 : 0)),
-                                     X0, c, vs);
-                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), 0.f);
+                    q0 = make_float4(__int_as_float(je0 | (q.near ? 1 << 30 : 0)), X0, c, vs);
+                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), __int_as_float(je1 - je0));
                     slow = EXACT || q.near;
                 }
+            }
+            {
+                // trip count shared by the two half-warps for this ball
+                const int spanq = pass ? __float_as_int(q1.w) : 0;
+                const int nl = (spanq + FSTR - 1) / FSTR;
+                const int nb = max(nl, __shfl_xor_sync(0xffffffffu, nl, FL));
+                q0.x = __int_as_float(__float_as_int(q0.x) | (nb << 15));
             }
             ws.rec[lane][0] = q0;
             ws.rec[lane][1] = q1;
@@ -354,20 +384,16 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 const int b = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const int src = h * FL + b;
-                // ball-uniform trip count: window <= 2 support a0 / (v dt) + 4
-                const float ab = __shfl_sync(0xffffffffu, cur.w, b);
-                const int niter =
-                    EXACT ? (s1 - s0 + FSTR + 1) / FSTR
-                          : (int)(ab * (2.f * sup / vdt) + 4.f + (float)(FSTR - 1)) / FSTR;
                 const float4 r0 = ws.rec[src][0];
+                const int span = __float_as_int(ws.rec[src][1].w);
                 if (!anyslow) {
-                    fwd_sweep_fast(tr, r0, niter, sub2, sub);
+                    fwd_sweep_fast(tr, r0, span, sub2, 2 * sub);
                 } else {
                     const bool sl = EXACT || ((__float_as_int(r0.x) >> 30) & 1);
                     if (__any_sync(0xffffffffu, sl))
-                        fwd_sweep_slow(tr, r0, ws.rec[src][1], niter, sub2, sub);
+                        fwd_sweep_slow(tr, r0, ws.rec[src][1], sub2, sub);
                     else
-                        fwd_sweep_fast(tr, r0, niter, sub2, sub);
+                        fwd_sweep_fast(tr, r0, span, sub2, 2 * sub);
                 }
                 __syncwarp();
             }
