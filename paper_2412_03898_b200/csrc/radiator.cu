@@ -35,7 +35,7 @@ constexpr int FSW = 2;              // sensors per warp (16 lanes each)
 constexpr int FL = 32 / FSW;        // lanes per (ball, sensor) pair
 constexpr int FSTR = 2 * FL;        // samples between a lane's successive pairs
 constexpr int FBATCH = 32 / FSW;    // balls per setup batch (one lane per pair)
-constexpr int FWD_TSEG_MAX = 1024;  // samples per time segment (private traces)
+constexpr int FWD_TSEG_MAX = 1536;  // samples per time segment (private traces)
 constexpr int TRACE_PAD = 8;        // floats after a trace (even-window overrun)
 
 struct FwdPlan {
@@ -44,15 +44,30 @@ struct FwdPlan {
     size_t partial_bytes, loss_bytes, prep_bytes;
 };
 
+// Segment length cap (samples); PC_FWD_TSEG overrides it for tuning sweeps.
+static int fwd_tseg_max() {
+    static int v = 0;
+    if (v == 0) {
+        const char* e = getenv("PC_FWD_TSEG");
+        const int x = e ? atoi(e) : 0;
+        v = (x >= 64 && x <= 8192) ? (x / 32) * 32 : FWD_TSEG_MAX;
+    }
+    return v;
+}
+
+static size_t fwd_smem_bytes(int Tseg);
+
 static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     FwdPlan p;
-    p.Tseg = T < FWD_TSEG_MAX ? ((T + 31) / 32) * 32 : FWD_TSEG_MAX;
+    const int tmax = fwd_tseg_max();
+    p.Tseg = T < tmax ? ((T + 31) / 32) * 32 : tmax;
     p.nseg = (T + p.Tseg - 1) / p.Tseg;
     const int64_t tiles = (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW);
     // CTAs with work (the active arrival range typically spans half of T);
-    // ask for >= 2 waves of resident CTAs (6 per SM) so the tail stays short
+    // ask for >= 2 waves of resident CTAs so the tail stays short
     const int64_t base = tiles * F * (p.nseg > 1 ? p.nseg / 2 : 1);
-    const int64_t want = 12LL * num_sms();
+    const int per_sm = (int)(228 * 1024 / (fwd_smem_bytes(p.Tseg) + 1024));
+    const int64_t want = 2LL * (per_sm < 1 ? 1 : per_sm > 16 ? 16 : per_sm) * num_sms();
     int64_t c = base >= want ? 1 : (want + base - 1) / base;
     const int64_t cmax = B / 256 > 1 ? B / 256 : 1;
     if (c > cmax) c = cmax;
@@ -68,8 +83,11 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     return p;
 }
 
+struct FwdRec {
+    float4 r0, r1;
+};
 struct FwdWarpSmem {                 // per-warp shared memory
-    float4 rec[32][2];               // pair records of the current batch (lane = pair)
+    FwdRec rec[32];                  // pair records of the current batch, [sensor slot][ball]
 };
 
 static size_t fwd_smem_bytes(int Tseg) {
@@ -171,70 +189,83 @@ struct FwdArgs {
 // half owns sample pairs (j, j+1), j = je0 + 2 sub + FSTR n, so each half's
 // float2 access is 128 contiguous bytes of its own trace (one conflict-free
 // wavefront).
-// One fast-path step: the sample pair at p (if the lane's window covers it),
-// then x advances one lane stride.
-__device__ __forceinline__ void fwd_step(float2* __restrict__ p, bool live, float2& x, float2 dx,
-                                         float2 cc) {
-    const float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
-    if (live) *p = ffma2(cc, v, *p);
-    x = fadd2(x, dx);
-}
+// Gaussian term of one sample pair: x 2^(-x^2)
+__device__ __forceinline__ float2 gterm(float2 x) { return fmul2(x, ex2n_2(fmul2(x, x))); }
 
-// Fast path.  Record r0 = {je0 | niter << 15, X0, c, vs} with niter the
-// larger trip count of the two half-warps (set up by the setup pass), and
-// r1.w = je1 - je0.  Each lane writes only inside its own window; unrolled by
-// 4, predicates compare the lane's remaining sample count with constants.
-__device__ __forceinline__ void fwd_sweep_fast(float* __restrict__ tr, float4 r0, int span,
-                                               float2 sub2, int sub2i) {
+// Record word 0: je0 | span << 15 | near << 30 (span = je1 - je0, even).
+__device__ __forceinline__ int rec_je0(int w) { return w & 0x7fff; }
+__device__ __forceinline__ int rec_span(int w) { return (w >> 15) & 0x7fff; }
+
+// Fast path.  r0 = {word, X0, c, dx} with X0 = x at je0 and dx = -FSTR s v dt.
+// Lane `sub` covers samples je0 + 2 sub + FSTR k; the first (span + 1) / FSTR
+// steps are inside the window on every lane of the half, at most one more is
+// live on the lower lanes.  trl = this half's trace at absolute sample 2 sub;
+// subq = 2 sub / FSTR (exact: x0 = X0 + subq dx = X0 - 2 sub s v dt).  In a
+// block of 4 steps x_k = x_b + k dx, x_b += 4 dx.
+__device__ __forceinline__ void fwd_sweep_fast(float2* __restrict__ trl, float4 r0, int sub2i,
+                                               float2 subq) {
     const int w = __float_as_int(r0.x);
-    const int je0 = w & 0x7fff;
-    const int niter = (w >> 15) & 0x7fff;
-    int rem = span - sub2i;                              // samples left from this lane's start
-    const float vs = r0.w;
+    const int span = rec_span(w);
+    const float2 dx = splat2(r0.w);
     const float2 cc = splat2(r0.z);
-    float2 x = ffma2(sub2, splat2(-vs), splat2(r0.y));
-    const float2 dx = splat2(-(float)FSTR * vs);
-    float2* p = reinterpret_cast<float2*>(tr + je0 + sub2i);
-    int n = niter;
-    for (; n >= 4; n -= 4, p += 4 * FL, rem -= 4 * FSTR) {
-        fwd_step(p, rem > 0, x, dx, cc);
-        fwd_step(p + FL, rem > FSTR, x, dx, cc);
-        fwd_step(p + 2 * FL, rem > 2 * FSTR, x, dx, cc);
-        fwd_step(p + 3 * FL, rem > 3 * FSTR, x, dx, cc);
+    float2 xb = ffma2(subq, dx, splat2(r0.y));
+    float2* p = trl + (rec_je0(w) >> 1);
+    const int nfull = (span + 1) / FSTR;
+    int n = nfull;
+    const float2 k2 = fadd2(dx, dx), k3 = fadd2(k2, dx), k4 = fadd2(k2, k2);
+    for (; n >= 4; n -= 4, p += 4 * FL) {
+        const float2 t0 = p[0], t1 = p[FL], t2 = p[2 * FL], t3 = p[3 * FL];
+        const float2 v0 = gterm(xb);
+        const float2 v1 = gterm(fadd2(xb, dx));
+        const float2 v2 = gterm(fadd2(xb, k2));
+        const float2 v3 = gterm(fadd2(xb, k3));
+        xb = fadd2(xb, k4);
+        p[0] = ffma2(cc, v0, t0);
+        p[FL] = ffma2(cc, v1, t1);
+        p[2 * FL] = ffma2(cc, v2, t2);
+        p[3 * FL] = ffma2(cc, v3, t3);
     }
-    if (n >= 2) {
-        fwd_step(p, rem > 0, x, dx, cc);
-        fwd_step(p + FL, rem > FSTR, x, dx, cc);
+    if (n & 2) {
+        const float2 t0 = p[0], t1 = p[FL];
+        const float2 v0 = gterm(xb);
+        const float2 v1 = gterm(fadd2(xb, dx));
+        xb = fadd2(xb, k2);
+        p[0] = ffma2(cc, v0, t0);
+        p[FL] = ffma2(cc, v1, t1);
         p += 2 * FL;
-        rem -= 2 * FSTR;
-        n -= 2;
     }
-    if (n) fwd_step(p, rem > 0, x, dx, cc);
+    if (n & 1) {
+        const float2 t0 = p[0];
+        const float2 v0 = gterm(xb);
+        xb = fadd2(xb, dx);
+        p[0] = ffma2(cc, v0, t0);
+        p += FL;
+    }
+    if (sub2i + nfull * FSTR < span) *p = ffma2(cc, gterm(xb), *p);
 }
 
 // Exact window / near field: x (and y) from the exact integer offset to the
 // wavefront sample jr every iteration (the window may start far from it).
-__device__ __forceinline__ void fwd_sweep_slow(float* __restrict__ tr, float4 r0, float4 r1,
-                                               float2 sub2, int sub) {
+// r1 = {X, Y at jr, jr, s v dt}.
+__device__ __forceinline__ void fwd_sweep_slow(float2* __restrict__ trl, float4 r0, float4 r1,
+                                               float2 sub2, int sub2i) {
     const int w = __float_as_int(r0.x);
-    const int je0 = w & 0x7fff;
+    const int je0 = rec_je0(w);
     const bool near = (w >> 30) & 1;
-    const int wl = __float_as_int(r1.w);               // je1 - je0 (0: empty pair)
-    const int nl = (wl - 2 * sub + FSTR - 1) / FSTR;
-    const int niter = max(nl, __shfl_xor_sync(0xffffffffu, nl, FL));
-    const float vs = r0.w;
+    const int nl = (rec_span(w) - sub2i + FSTR - 1) / FSTR;
+    const float vs = r1.w;
     const float2 cc = splat2(r0.z);
     const int jr = __float_as_int(r1.z);
     float2 k = fadd2(sub2, splat2((float)(je0 - jr)));
-    float2* p = reinterpret_cast<float2*>(tr + je0) + sub;
-    for (int n = 0; n < niter; ++n, p += FL) {
+    float2* p = trl + (je0 >> 1);
+    for (int n = 0; n < nl; ++n, p += FL) {
         const float2 x = ffma2(k, splat2(-vs), splat2(r1.x));
         float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
         if (near) {
             const float2 y = ffma2(k, splat2(vs), splat2(r1.y));
             v = ffma2(y, ex2n_2(fmul2(y, y)), v);
         }
-        if (n < nl) *p = ffma2(cc, v, *p);
+        *p = ffma2(cc, v, *p);
         k = fadd2(k, splat2((float)FSTR));
     }
 }
@@ -316,7 +347,6 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     const int w0 = seg == 0 ? 0 : s0;               // output range this warp writes
     const int w1 = seg == nseg_w - 1 ? T : s1;
     for (int j = lane; j < FSW * TP; j += 32) traces[j] = 0.f;
-    float* tr = traces + h * TP - s0;               // this half's sensor, absolute index
 
     const float d_lo = (float)(a.ac.v * (a.ac.t0 + (double)s0 * a.ac.dt)) - 2.f * a.ac.vdt;
     const float d_hi = (float)(a.ac.v * (a.ac.t0 + (double)(s1 - 1) * a.ac.dt)) + 2.f * a.ac.vdt;
@@ -327,6 +357,11 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     const float vdt = a.ac.vdt;
     const bool scan = s1 > s0 || (seg == 0 && dmin_box < 1e-3f);
     const float2 sub2 = make_float2((float)(2 * sub), (float)(2 * sub + 1));
+    const float2 subq = make_float2((float)(2 * sub) / FSTR, (float)(2 * sub + 1) / FSTR);
+    // this half's trace at absolute sample 2 sub (s0 and je0 are even; only
+    // in-window samples are ever addressed)
+    float2* trl = reinterpret_cast<float2*>(traces + h * TP) + (sub - (s0 >> 1));
+    FwdRec* recs = &ws.rec[h * FBATCH];
     __syncwarp();
 
     if (scan) {
@@ -362,38 +397,34 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     const int je0 = q.jl & ~1;
                     const int je1 = (q.jh + 1) & ~1;
                     const float X0 = fmaf((float)(q.jr - je0), vs, q.X);
-                    q0 = make_float4(__int_as_float(je0 | (q.near ? 1 << 30 : 0)), X0, c, vs);
-                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), __int_as_float(je1 - je0));
+                    q0 = make_float4(
+                        __int_as_float(je0 | ((je1 - je0) << 15) | (q.near ? 1 << 30 : 0)), X0, c,
+                        -(float)FSTR * vs);
+                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), vs);
                     slow = EXACT || q.near;
                 }
             }
-            {
-                // trip count shared by the two half-warps for this ball
-                const int spanq = pass ? __float_as_int(q1.w) : 0;
-                const int nl = (spanq + FSTR - 1) / FSTR;
-                const int nb = max(nl, __shfl_xor_sync(0xffffffffu, nl, FL));
-                q0.x = __int_as_float(__float_as_int(q0.x) | (nb << 15));
-            }
-            ws.rec[lane][0] = q0;
-            ws.rec[lane][1] = q1;
+            // compact: balls with a live pair for either sensor, in batch order
             const unsigned pm = __ballot_sync(0xffffffffu, pass);
             const bool anyslow = __any_sync(0xffffffffu, slow);
-            unsigned mask = (pm | (pm >> FL)) & ((1u << FL) - 1u);   // balls with any pair
+            const unsigned bm = (pm | (pm >> FL)) & ((1u << FL) - 1u);
+            if ((bm >> sub) & 1u) {
+                const int pos = __popc(bm & ((1u << sub) - 1u));
+                recs[pos].r0 = q0;
+                recs[pos].r1 = q1;
+            }
+            const int nb = __popc(bm);
             __syncwarp();
-            while (mask) {
-                const int b = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int src = h * FL + b;
-                const float4 r0 = ws.rec[src][0];
-                const int span = __float_as_int(ws.rec[src][1].w);
+            for (int k = 0; k < nb; ++k) {
+                const float4 r0 = recs[k].r0;
                 if (!anyslow) {
-                    fwd_sweep_fast(tr, r0, span, sub2, 2 * sub);
+                    fwd_sweep_fast(trl, r0, 2 * sub, subq);
                 } else {
                     const bool sl = EXACT || ((__float_as_int(r0.x) >> 30) & 1);
                     if (__any_sync(0xffffffffu, sl))
-                        fwd_sweep_slow(tr, r0, ws.rec[src][1], sub2, sub);
+                        fwd_sweep_slow(trl, r0, recs[k].r1, sub2, 2 * sub);
                     else
-                        fwd_sweep_fast(tr, r0, span, sub2, 2 * sub);
+                        fwd_sweep_fast(trl, r0, 2 * sub, subq);
                 }
                 __syncwarp();
             }
@@ -778,7 +809,7 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         const size_t smem = fwd_smem_bytes(p.Tseg);
         static bool attr_set = false;
         if (!attr_set) {
-            const int mx = (int)fwd_smem_bytes(FWD_TSEG_MAX);
+            const int mx = (int)fwd_smem_bytes(fwd_tseg_max());
             cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             attr_set = true;
