@@ -153,6 +153,17 @@ int pc_forward_traces(const double *mu_t, const float *a0_t,
                       int64_t *coincident, void *workspace,
                       size_t workspace_bytes, pc_stream_t stream);
 
+/* The residual/loss epilogue of pc_forward_traces as its own call, for
+ * callers that overlap the observed-trace upload with the forward sweep
+ * (reconstruction.py:312-313): out = predicted - observed (out may alias
+ * predicted) and, if loss_per_frame is non-NULL, loss_per_frame[f] =
+ * 0.5*sum r^2 (f64, fixed-order reduction; loss_partial = F*M doubles of
+ * scratch). */
+int pc_residual_loss(const float *predicted, const float *observed, float *out,
+                     double *loss_partial, double *loss_per_frame,
+                     int32_t n_frames, int32_t n_sensors, int32_t n_samples,
+                     pc_stream_t stream);
+
 /* Replaces radiator.py:121-174 _residual_state_grads (+ frame_state_grads
  * :219-242), batched over F frames: G (F,B,5) f32 is overwritten with the
  * gradient of 0.5*||residual||^2 w.r.t. (a0_t, p0_t, mu_t). */

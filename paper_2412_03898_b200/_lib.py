@@ -69,6 +69,8 @@ SIGNATURES = {
                                     c_size_t, _P]),
     "pc_residual_state_grads": (c_int32, [_P, _P, _P, c_int64, c_int32,
                                           POINTER(PcArray), _P, _P, _P, _P]),
+    "pc_residual_loss": (c_int32, [_P, _P, _P, _P, _P, c_int32, c_int32,
+                                   c_int32, _P]),
     "pc_l2_loss": (c_int32, [_P, _P, c_int64, _P, _P]),
     "pc_check_finite": (c_int32, [_P, c_int32, POINTER(c_int64), _P, _P]),
     "pc_adam_segments": (c_int32, [_P, _P, _P, _P, c_int32, POINTER(c_int64),

@@ -462,9 +462,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
 }
 
 // Chunk combine (fixed chunk order) + residual + per-trace loss partial.
-__global__ void __launch_bounds__(256) k_forward_finish(const float* __restrict__ partial,
+// (out may alias partial when nchunk == 1: element-wise, same thread)
+__global__ void __launch_bounds__(256) k_forward_finish(const float* partial,
                                                         const float* __restrict__ obs,
-                                                        float* __restrict__ out,
+                                                        float* out,
                                                         double* __restrict__ loss, int nchunk,
                                                         int F, int M, int T) {
     const int m = blockIdx.x, f = blockIdx.y;
@@ -845,6 +846,22 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         const int per_frame = (n_balls > 0 && p.nchunk == 1) ? M * p.nseg : M;
         k_loss_reduce<<<F, 256, 0, st>>>(lpart, per_frame, loss_per_frame);
     }
+    return last_status();
+}
+
+extern "C" int pc_residual_loss(const float* predicted, const float* observed, float* out,
+                                double* loss_partial, double* loss_per_frame, int32_t n_frames,
+                                int32_t n_sensors, int32_t n_samples, pc_stream_t stream) {
+    if (n_frames < 0 || n_sensors < 0 || n_samples < 0) return PC_ERR_ARGUMENT;
+    if (n_frames == 0 || n_sensors == 0 || n_samples == 0) return PC_OK;
+    if (!predicted || !observed || !out || (loss_per_frame && !loss_partial))
+        return PC_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    k_forward_finish<<<dim3(n_sensors, n_frames), 256, 0, st>>>(
+        predicted, observed, out, loss_per_frame ? loss_partial : nullptr, 1, n_frames, n_sensors,
+        n_samples);
+    if (loss_per_frame)
+        k_loss_reduce<<<n_frames, 256, 0, st>>>(loss_partial, n_sensors, loss_per_frame);
     return last_status();
 }
 

@@ -39,7 +39,7 @@ from .deformation import (DeviceCloud, deform_backward_device,
                           deform_states_device)
 from .distributed import allreduce_iteration, frame_shard, shard_range
 from .radiator import (DeviceArray, forward_device, raise_if_coincident,
-                       state_grads_device, to_device)
+                       residual_loss_device, state_grads_device, to_device)
 
 GROUP_ORDER = ("pressure", "std", "coords", "deform")
 GROUP_OF = {"p0": "pressure", "a0": "std", "mu": "coords", "theta": "deform",
@@ -192,6 +192,29 @@ class IterationEngine:
                                 device=self.device)
         self.loss_total = torch.zeros(1, dtype=torch.float64,
                                       device=self.device)
+        self.host_observed = None
+        self._copy_stream = None
+
+    def stream_observed_from(self, host):
+        """Upload the observed traces from pinned host memory every iteration
+        (frames of the minibatch only), overlapped with the deformation and
+        the forward sweep: the copy runs on a side stream and only the
+        residual/loss epilogue (pc_residual_loss) waits for it.  `host` is a
+        pinned, contiguous CPU float32 tensor (F_all, M_local, T); None turns
+        streaming off (the device copy made at construction is used)."""
+        if host is not None:
+            if not (isinstance(host, torch.Tensor) and host.device.type == "cpu"
+                    and host.is_pinned() and host.is_contiguous()
+                    and host.dtype == torch.float32):
+                raise ValueError("host observed must be a pinned contiguous "
+                                 "float32 CPU tensor")
+            if tuple(host.shape) != tuple(self.observed.shape):
+                raise ValueError(f"host observed shape {tuple(host.shape)} != "
+                                 f"{tuple(self.observed.shape)}")
+            if self._copy_stream is None:
+                self._copy_stream = torch.cuda.Stream(device=self.device)
+        self.host_observed = host
+        self._graph = None
 
     # ------------------------------------------------------------ buffers
     def _ensure_buffers(self, F: int):
@@ -209,6 +232,7 @@ class IterationEngine:
         ws = self.darr.workspace_bytes(max(B, 1), F)
         self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
         self.obs_stage = None
+        self.loss_part = torch.empty(F * M, dtype=torch.float64, device=dev)
         self._bufs_F = F
         self._graph = None
 
@@ -218,16 +242,34 @@ class IterationEngine:
         return np.asarray(frames, dtype=np.int64)
 
     # ------------------------------------------------------------ compute
-    def _launch_compute(self, obs):
-        """deform -> forward+loss -> adjoint -> deformation backward."""
+    def _launch_compute(self, obs, host_src=None):
+        """deform -> forward+loss -> adjoint -> deformation backward.
+
+        With host_src (pinned host frames), obs is filled from it on the side
+        stream while deform + forward run; the residual/loss epilogue joins."""
         cfg = self.cfg
+        cur = torch.cuda.current_stream()
+        if host_src is not None:
+            side = self._copy_stream
+            side.wait_stream(cur)       # obs no longer read by the last step
+            with torch.cuda.stream(side):
+                for dst, src in host_src:
+                    dst.copy_(src, non_blocking=True)
         self.coinc.fill_(_lib.INT64_MAX)
         deform_states_device(self.dcloud, self.t_dev, cfg.coord_mode,
                              cfg.a0_floor, self.mu_t, self.a0_t, self.p0_t,
                              self.H)
-        forward_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
-                       observed=obs, out=self.resid, loss=self.loss_f,
-                       coincident=self.coinc, workspace=self.ws)
+        if host_src is None:
+            forward_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
+                           observed=obs, out=self.resid, loss=self.loss_f,
+                           coincident=self.coinc, workspace=self.ws)
+        else:
+            forward_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
+                           observed=None, out=self.resid,
+                           coincident=self.coinc, workspace=self.ws)
+            cur.wait_stream(self._copy_stream)
+            residual_loss_device(self.resid, obs, out=self.resid,
+                                 loss=self.loss_f, partial=self.loss_part)
         state_grads_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
                            self.resid, G=self.G, coincident=self.coinc)
         deform_backward_device(self.dcloud, self.t_dev, cfg.coord_mode,
@@ -246,15 +288,24 @@ class IterationEngine:
         self._ensure_buffers(F)
         contiguous = np.array_equal(local, np.arange(local[0],
                                                      local[0] + F))
+        host = self.host_observed
+        host_src = None
         if contiguous:
-            obs = self.observed[int(local[0]):int(local[0]) + F]
+            lo = int(local[0])
+            obs = self.observed[lo:lo + F]
+            if host is not None:
+                host_src = [(obs, host[lo:lo + F])]
         else:
             if self.obs_stage is None:
                 self.obs_stage = torch.empty_like(self.observed[:F])
-            idx = torch.as_tensor(local, device=self.device)
-            torch.index_select(self.observed, 0, idx, out=self.obs_stage)
             obs = self.obs_stage
-        key = tuple(int(k) for k in local)
+            if host is not None:
+                host_src = [(obs[i], host[int(f)]) for i, f in enumerate(local)]
+            else:
+                idx = torch.as_tensor(local, device=self.device)
+                torch.index_select(self.observed, 0, idx, out=self.obs_stage)
+        key = (tuple(int(k) for k in local),
+               None if host is None else host.data_ptr())
         if self.use_graph and self._graph is not None \
                 and self._graph_frames == key:
             self._graph.replay()
@@ -264,19 +315,19 @@ class IterationEngine:
         if self.use_graph and contiguous:
             # warm once eagerly (lazy init inside torch / the driver), then
             # capture the fixed launch sequence and replay it from now on
-            self._launch_compute(obs)
+            self._launch_compute(obs, host_src)
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):
-                    self._launch_compute(obs)
+                    self._launch_compute(obs, host_src)
             torch.cuda.current_stream().wait_stream(s)
             self._graph, self._graph_frames = g, key
             self._graph.replay()
         else:
             self._graph = None      # t_dev / obs changed under the graph
-            self._launch_compute(obs)
+            self._launch_compute(obs, host_src)
 
     def allreduce(self) -> None:
         if self.world > 1:

@@ -132,6 +132,26 @@ def forward_device(darr: DeviceArray, mu_t, a0_t, p0_t, observed=None,
     return out, loss, coincident
 
 
+def residual_loss_device(predicted, observed, out=None, loss=None,
+                         partial=None):
+    """pc_residual_loss: out = predicted - observed (in place when out is
+    predicted), loss (F,) f64 = 0.5 * sum r^2 per frame."""
+    lib = _lib.load_library()
+    F, M, T = (int(x) for x in predicted.shape)
+    dev = predicted.device
+    if out is None:
+        out = predicted
+    if loss is None:
+        loss = torch.empty(F, dtype=torch.float64, device=dev)
+    if partial is None or partial.numel() < F * M:
+        partial = torch.empty(F * M, dtype=torch.float64, device=dev)
+    _lib.check(lib.pc_residual_loss(
+        _lib.ptr(predicted), _lib.ptr(observed), _lib.ptr(out),
+        _lib.ptr(partial), _lib.ptr(loss), F, M, T, _lib.stream()),
+        "pc_residual_loss")
+    return out, loss
+
+
 def state_grads_device(darr: DeviceArray, mu_t, a0_t, p0_t, residual,
                        G=None, coincident=None):
     """pc_residual_state_grads: G (F,B,5) f32 from residual (F,M,T)."""
