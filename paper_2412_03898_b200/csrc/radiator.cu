@@ -192,7 +192,8 @@ struct FwdArgs {
 // Gaussian term of one sample pair: x 2^(-x^2)
 __device__ __forceinline__ float2 gterm(float2 x) { return fmul2(x, ex2n_2(fmul2(x, x))); }
 
-// Record word 0: je0 | span << 15 | near << 30 (span = je1 - je0, even).
+// Record word 0: je0 | span << 15 | near << 30 | recur << 31 (span = je1 - je0,
+// even; recur: the ball's Gaussian may be stepped by recurrence, recur_ok).
 __device__ __forceinline__ int rec_je0(int w) { return w & 0x7fff; }
 __device__ __forceinline__ int rec_span(int w) { return (w >> 15) & 0x7fff; }
 
@@ -244,16 +245,70 @@ __device__ __forceinline__ void fwd_sweep_fast(float2* __restrict__ trl, float4 
     if (sub2i + nfull * FSTR < span) *p = ffma2(cc, gterm(xb), *p);
 }
 
+// Fast path by recurrence (the adjoint's scheme): with D = FSTR s v dt,
+// e = 2^-x^2 steps as e <- e g, g <- g h (g = 2^(2 D x - D^2), h = 2^(-2 D^2)),
+// so MUFU runs only at the lane's first sample.  Same lane layout as
+// fwd_sweep_fast; r0.w = dx = -D, h from the record.
+__device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4 r0, float h,
+                                                int sub2i, float2 subq) {
+    const int w = __float_as_int(r0.x);
+    const int span = rec_span(w);
+    const float2 dx = splat2(r0.w);
+    const float2 cc = splat2(r0.z);
+    float2 x = ffma2(subq, dx, splat2(r0.y));
+    float2 e = ex2n_2(fmul2(x, x));
+    float2 g = ex2_2(ffma2(x, splat2(-2.f * r0.w), splat2(-r0.w * r0.w)));
+    const float2 h2 = splat2(h);
+    float2* p = trl + (rec_je0(w) >> 1);
+    const int nfull = (span + 1) / FSTR;
+    int n = nfull;
+#define PC_FWD_RSTEP(V)   \
+    V = fmul2(x, e);      \
+    e = fmul2(e, g);      \
+    g = fmul2(g, h2);     \
+    x = fadd2(x, dx);
+    for (; n >= 4; n -= 4, p += 4 * FL) {
+        const float2 t0 = p[0], t1 = p[FL], t2 = p[2 * FL], t3 = p[3 * FL];
+        float2 v0, v1, v2, v3;
+        PC_FWD_RSTEP(v0)
+        PC_FWD_RSTEP(v1)
+        PC_FWD_RSTEP(v2)
+        PC_FWD_RSTEP(v3)
+        p[0] = ffma2(cc, v0, t0);
+        p[FL] = ffma2(cc, v1, t1);
+        p[2 * FL] = ffma2(cc, v2, t2);
+        p[3 * FL] = ffma2(cc, v3, t3);
+    }
+    if (n & 2) {
+        const float2 t0 = p[0], t1 = p[FL];
+        float2 v0, v1;
+        PC_FWD_RSTEP(v0)
+        PC_FWD_RSTEP(v1)
+        p[0] = ffma2(cc, v0, t0);
+        p[FL] = ffma2(cc, v1, t1);
+        p += 2 * FL;
+    }
+    if (n & 1) {
+        const float2 t0 = p[0];
+        float2 v0;
+        PC_FWD_RSTEP(v0)
+        p[0] = ffma2(cc, v0, t0);
+        p += FL;
+    }
+#undef PC_FWD_RSTEP
+    if (sub2i + nfull * FSTR < span) *p = ffma2(cc, fmul2(x, e), *p);
+}
+
 // Exact window / near field: x (and y) from the exact integer offset to the
 // wavefront sample jr every iteration (the window may start far from it).
-// r1 = {X, Y at jr, jr, s v dt}.
+// r1 = {X, Y at jr, jr, h}; s v dt = -r0.w / FSTR (exact).
 __device__ __forceinline__ void fwd_sweep_slow(float2* __restrict__ trl, float4 r0, float4 r1,
                                                float2 sub2, int sub2i) {
     const int w = __float_as_int(r0.x);
     const int je0 = rec_je0(w);
     const bool near = (w >> 30) & 1;
     const int nl = (rec_span(w) - sub2i + FSTR - 1) / FSTR;
-    const float vs = r1.w;
+    const float vs = r0.w * (-1.f / FSTR);
     const float2 cc = splat2(r0.z);
     const int jr = __float_as_int(r1.z);
     float2 k = fadd2(sub2, splat2((float)(je0 - jr)));
@@ -400,9 +455,16 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     q0 = make_float4(
                         __int_as_float(je0 | ((je1 - je0) << 15) | (q.near ? 1 << 30 : 0)), X0, c,
                         -(float)FSTR * vs);
-                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), vs);
+                    const float D = (float)FSTR * vs;
+                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), ex2(-2.f * D * D));
                     slow = EXACT || q.near;
                 }
+            }
+            if (!EXACT) {
+                // per ball (both sensors of the warp agree): recurrence stepping
+                const float vsb = vdt * scale_of(cur.w);
+                if (recur_ok((float)FSTR * vsb, vsb, sup))
+                    q0.x = __int_as_float(__float_as_int(q0.x) | (int)0x80000000u);
             }
             // compact: balls with a live pair for either sensor, in batch order
             const unsigned pm = __ballot_sync(0xffffffffu, pass);
@@ -417,15 +479,18 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             __syncwarp();
             for (int k = 0; k < nb; ++k) {
                 const float4 r0 = recs[k].r0;
-                if (!anyslow) {
-                    fwd_sweep_fast(trl, r0, 2 * sub, subq);
-                } else {
-                    const bool sl = EXACT || ((__float_as_int(r0.x) >> 30) & 1);
-                    if (__any_sync(0xffffffffu, sl))
-                        fwd_sweep_slow(trl, r0, recs[k].r1, sub2, 2 * sub);
-                    else
-                        fwd_sweep_fast(trl, r0, 2 * sub, subq);
+                const bool rec = __float_as_int(r0.x) < 0;
+                bool sl = false;
+                if (anyslow) {
+                    sl = EXACT || ((__float_as_int(r0.x) >> 30) & 1);
+                    sl = __any_sync(0xffffffffu, sl);
                 }
+                if (sl)
+                    fwd_sweep_slow(trl, r0, recs[k].r1, sub2, 2 * sub);
+                else if (rec)
+                    fwd_sweep_recur(trl, r0, recs[k].r1.w, 2 * sub, subq);
+                else
+                    fwd_sweep_fast(trl, r0, 2 * sub, subq);
                 __syncwarp();
             }
         }
