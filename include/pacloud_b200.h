@@ -173,6 +173,22 @@ int pc_residual_state_grads(const double *mu_t, const float *a0_t,
                             const float *residual, float *G,
                             int64_t *coincident, pc_stream_t stream);
 
+/* ---- evaluation --------------------------------------------------------- */
+
+/* Scratch bytes of pc_voxelize. */
+size_t pc_voxelize_workspace_bytes(int64_t n_balls);
+
+/* Replaces evaluation.py:46-93 _splat_balls / voxelize: out (nx,ny,nz) f32,
+ * C order, = sum_b p0_b exp(-|x - mu_b|^2 / (2 a0_b^2)) at voxel centres
+ * origin + i*spacing, limited to each ball's support cube unless exact.
+ * mu (B,3), a0, p0 (B) f64 on the device; origin[3] and dims[3] host arrays
+ * (dims <= 32767).  bad_a0: device int32, set to 1 if any a0 <= 0. */
+int pc_voxelize(const double *mu, const double *a0, const double *p0,
+                int64_t n_balls, const double *origin, double spacing,
+                const int32_t *dims, double support_sigmas, int32_t exact,
+                float *out, int32_t *bad_a0, void *workspace,
+                size_t workspace_bytes, pc_stream_t stream);
+
 /* ---- loss and optimiser ------------------------------------------------- */
 
 /* Replaces reconstruction.py:28-35 l2_loss: out[0] = 0.5*sum (p-o)^2 (f64,

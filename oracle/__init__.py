@@ -66,6 +66,10 @@ def _load():
             dp, dp, i64, dp, i64, ctypes.c_double, ctypes.c_double,
             ctypes.c_double, i64, ctypes.c_double, ctypes.c_int, ctypes.c_int]
         lib.oracle_support_samples.restype = i64
+        lib.oracle_voxelize.argtypes = [
+            dp, dp, dp, i64, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_double, i64, i64, i64, ctypes.c_double,
+            ctypes.c_int, dp, ctypes.c_int]
         lib.oracle_max_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -487,3 +491,108 @@ def apply_densify(params: dict, index, is_child, split, keep,
         shift = np.where(is_child, child_shift * out["a0"], 0.0)
         out["mu"][:, 0] = out["mu"][:, 0] + shift
     return out
+
+
+# --------------------------------------------------------------------------
+# static stage -- reconstruction.py:160-231
+# --------------------------------------------------------------------------
+
+def lattice_1d(lo, hi, pitch):
+    """geometry.py:121-126."""
+    n = max(1, int(np.floor((hi - lo) / pitch + 1e-12)))
+    return 0.5 * (lo + hi) - 0.5 * (n - 1) * pitch + pitch * np.arange(n)
+
+
+def box_lattice(lo, hi, pitch):
+    """geometry.py:129-132 (x slowest)."""
+    ax = [lattice_1d(lo[k], hi[k], pitch) for k in range(3)]
+    return np.stack(np.meshgrid(*ax, indexing="ij"), -1).reshape(-1, 3)
+
+
+def static_reconstruct(observed, array, cfg, roi_lo, roi_hi, losses=None,
+                       threads=0):
+    """Lattice init, then per iteration forward -> loss -> adjoint -> Adam
+    (pressure, std, coords) -> floors -> prune every prune_every.
+    Returns (p0, a0, mu) float64 arrays."""
+    observed = np.asarray(observed, dtype=np.float64)
+    mu = box_lattice(roi_lo, roi_hi, cfg.init_pitch)
+    a0 = np.full(len(mu), cfg.init_pitch / 2.0)
+    peak = float(np.max(np.abs(observed))) if observed.size else 0.0
+    p0 = np.full(len(mu), cfg.init_p0_scale * peak)
+    mom = {k: Moments(np.zeros_like(v), np.zeros_like(v))
+           for k, v in (("p0", p0), ("a0", a0), ("mu", mu))}
+    for it in range(cfg.static_iters):
+        lr = {g: scheduled_lr(getattr(cfg, "lr_" + g), it, cfg.step_size,
+                              cfg.drop_rate)
+              for g in ("pressure", "std", "coords")}
+        st = States(a0, p0, mu)
+        r = forward_frame(st, array, cfg.support_sigmas, cfg.exact_forward,
+                          threads) - observed
+        loss = 0.5 * float(np.sum(r * r))
+        if not np.isfinite(loss):
+            raise RuntimeError(f"non-finite loss at iteration {it}")
+        if losses is not None:
+            losses.append(loss)
+        G = frame_state_grads(st, array, r, cfg.support_sigmas,
+                              cfg.exact_forward, threads)
+        step = adam_step if cfg.optimizer == "adam" else None
+        for key, arr, g, grp in (("p0", p0, G[:, 1], "pressure"),
+                                 ("a0", a0, G[:, 0], "std"),
+                                 ("mu", mu, G[:, 2:5], "coords")):
+            if step is not None:
+                step(arr, g, mom[key], lr[grp], grp)
+            else:
+                sgd_step(arr, g, lr[grp], grp)
+        np.maximum(p0, cfg.p0_floor, out=p0)
+        np.maximum(a0, cfg.a0_floor, out=a0)
+        if (it + 1) % cfg.prune_every == 0:
+            keep = prune_keep(p0, cfg.prune_threshold)
+            if not keep.any():
+                raise RuntimeError("all balls pruned")
+            if not keep.all():
+                p0, a0, mu = p0[keep], a0[keep], mu[keep]
+                for m in mom.values():
+                    m.m, m.v = m.m[keep], m.v[keep]
+    return p0, a0, mu
+
+
+# ---------------------------------------------------------------- evaluation
+
+def voxelize(mu, a0, p0, origin, spacing, dims, support_sigmas=6.0,
+             exact=False, threads=0) -> np.ndarray:
+    """evaluation.py:46-93: (nx, ny, nz) float64 Gaussian field at voxel
+    centres origin + i * spacing (C restatement of _splat_balls)."""
+    mu = np.ascontiguousarray(mu, dtype=np.float64).reshape(-1, 3)
+    a0 = np.ascontiguousarray(a0, dtype=np.float64).ravel()
+    p0 = np.ascontiguousarray(p0, dtype=np.float64).ravel()
+    if len(a0) and np.any(a0 <= 0):
+        raise ValueError("all a0_t must be > 0")
+    dims = tuple(int(d) for d in dims)
+    out = np.zeros(dims)
+    o = np.asarray(origin, dtype=np.float64)
+    _load().oracle_voxelize(_dp(mu), _dp(a0), _dp(p0), len(a0), o[0], o[1],
+                            o[2], float(spacing), dims[0], dims[1], dims[2],
+                            float(support_sigmas), int(bool(exact)), _dp(out),
+                            int(threads))
+    return out
+
+
+def ssim(a, b, data_range=1.0, window=11, sigma=1.5, k1=0.01, k2=0.03):
+    """evaluation.py:142-184: mean SSIM over fully contained Gaussian
+    windows (numpy, float64)."""
+    from numpy.lib.stride_tricks import sliding_window_view
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    r = np.arange(window, dtype=np.float64) - (window - 1) / 2.0
+    g = np.exp(-0.5 * (r / sigma) ** 2)
+    w = np.outer(g, g)
+    w /= w.sum()
+
+    def filt(img):
+        return np.einsum("ijkl,kl->ij", sliding_window_view(img, w.shape), w)
+    c1, c2 = (k1 * data_range) ** 2, (k2 * data_range) ** 2
+    ma, mb = filt(a), filt(b)
+    va, vb = filt(a * a) - ma * ma, filt(b * b) - mb * mb
+    cov = filt(a * b) - ma * mb
+    return float(np.mean((2 * ma * mb + c1) * (2 * cov + c2) /
+                         ((ma * ma + mb * mb + c1) * (va + vb + c2))))

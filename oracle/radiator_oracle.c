@@ -187,3 +187,52 @@ int oracle_max_threads(void)
     return 1;
 #endif
 }
+
+/* evaluation.py:46-74 _splat_balls: out (nx,ny,nz) += p0 exp(-d^2/(2 a0^2))
+ * over each ball's support cube (|x - mu_x| <= reach per x plane, ceil /
+ * floor index ranges along y and z), every voxel when exact.  x planes in
+ * parallel, balls in index order per plane, float64 throughout. */
+void oracle_voxelize(const double *mu, const double *a0, const double *p0,
+                     int64_t n_balls, double ox, double oy, double oz,
+                     double sp, int64_t nx, int64_t ny, int64_t nz,
+                     double support, int exact, double *out, int n_threads)
+{
+#ifdef _OPENMP
+    if (n_threads > 0) omp_set_num_threads(n_threads);
+#else
+    (void)n_threads;
+#endif
+    int64_t ix;
+#pragma omp parallel for schedule(static)
+    for (ix = 0; ix < nx; ++ix) {
+        const double x = ox + ix * sp;
+        for (int64_t b = 0; b < n_balls; ++b) {
+            const double reach = support * a0[b];
+            const double mx = mu[3 * b], my = mu[3 * b + 1], mz = mu[3 * b + 2];
+            if (!exact && fabs(x - mx) > reach) continue;
+            int64_t ylo = 0, yhi = ny, zlo = 0, zhi = nz;
+            if (!exact) {
+                ylo = (int64_t)ceil((my - reach - oy) / sp);
+                yhi = (int64_t)floor((my + reach - oy) / sp) + 1;
+                zlo = (int64_t)ceil((mz - reach - oz) / sp);
+                zhi = (int64_t)floor((mz + reach - oz) / sp) + 1;
+                if (ylo < 0) ylo = 0;
+                if (yhi > ny) yhi = ny;
+                if (zlo < 0) zlo = 0;
+                if (zhi > nz) zhi = nz;
+            }
+            const double k = 1.0 / (2.0 * a0[b] * a0[b]);
+            const double dx2 = (x - mx) * (x - mx);
+            for (int64_t iy = ylo; iy < yhi; ++iy) {
+                const double y = oy + iy * sp;
+                const double dy2 = (y - my) * (y - my);
+                double *row = out + (ix * ny + iy) * nz;
+                for (int64_t iz = zlo; iz < zhi; ++iz) {
+                    const double z = oz + iz * sp;
+                    const double dz2 = (z - mz) * (z - mz);
+                    row[iz] += p0[b] * exp(-(dx2 + dy2 + dz2) * k);
+                }
+            }
+        }
+    }
+}

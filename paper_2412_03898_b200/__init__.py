@@ -9,13 +9,20 @@ include/pacloud_b200.h):
     reconstruction.l2_loss / adam_step / sgd_step / ParamGroup(s) /
         dynamic_reconstruct
     engine.IterationEngine      fused multi-frame iteration (+ NCCL sharding)
+    geometry.simulate_dataset / build_phantom / spherical_array (target
+        synthesis on the forward kernel)
+    evaluation.voxelize / map_project / ssim / eval_report
 """
 
-from .core import (AdamState, BallStateAtT, CloudGrads, CloudState,
+from .core import (AdamState, BallStateAtT, Box, CloudGrads, CloudState,
                    CloudStateGrad, DynamicCloud, ReconConfig, SensorArray,
-                   SignalSet, default_basis_grid, frame_times)
+                   SignalSet, VoxelGrid, default_basis_grid, frame_times)
 from .deformation import cloud_state_grads, cloud_states_at
 from .engine import IterationEngine
+from .evaluation import (GridSpec, eval_report, format_report, map_project,
+                         ssim, voxelize)
+from .geometry import (Phantom, PhantomSpec, build_phantom, fibonacci_sphere,
+                       simulate_dataset, spherical_array)
 from .radiator import (accumulate_frame_grads, forward_frame,
                        frame_state_grads)
 from .reconstruction import (ParamGroup, ParamGroups, adam_step,
@@ -31,4 +38,7 @@ __all__ = [
     "cloud_states_at", "IterationEngine", "accumulate_frame_grads",
     "forward_frame", "frame_state_grads", "ParamGroup", "ParamGroups",
     "adam_step", "dynamic_reconstruct", "l2_loss", "scheduled_lr", "sgd_step",
+    "Box", "VoxelGrid", "GridSpec", "eval_report", "format_report",
+    "map_project", "ssim", "voxelize", "Phantom", "PhantomSpec",
+    "build_phantom", "fibonacci_sphere", "simulate_dataset", "spherical_array",
 ]

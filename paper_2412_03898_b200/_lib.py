@@ -71,6 +71,10 @@ SIGNATURES = {
                                           POINTER(PcArray), _P, _P, _P, _P]),
     "pc_residual_loss": (c_int32, [_P, _P, _P, _P, _P, c_int32, c_int32,
                                    c_int32, _P]),
+    "pc_voxelize_workspace_bytes": (c_size_t, [c_int64]),
+    "pc_voxelize": (c_int32, [_P, _P, _P, c_int64, POINTER(c_double),
+                              c_double, POINTER(c_int32), c_double, c_int32,
+                              _P, _P, _P, c_size_t, _P]),
     "pc_l2_loss": (c_int32, [_P, _P, c_int64, _P, _P]),
     "pc_check_finite": (c_int32, [_P, c_int32, POINTER(c_int64), _P, _P]),
     "pc_adam_segments": (c_int32, [_P, _P, _P, _P, c_int32, POINTER(c_int64),

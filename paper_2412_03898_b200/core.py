@@ -1,6 +1,8 @@
 """Hot-path domain types, mirroring the reference's names and fields.
 
-Mirrors (pkg/src/pacloud): ``SensorArray`` (core.py:295-354), ``SignalSet``
+Mirrors (pkg/src/pacloud): ``Box`` (core.py:35-70), ``GaussBall``
+(core.py:74-101), ``VoxelGrid``
+(core.py:418-446), ``SensorArray`` (core.py:295-354), ``SignalSet``
 (core.py:366-414), ``DynamicCloud`` (core.py:166-259), ``ReconConfig``
 (core.py:448-502), ``frame_times`` (core.py:357-363),
 ``default_basis_grid`` (core.py:152-163), ``CloudState`` /
@@ -24,6 +26,106 @@ CHANNELS = ("a0", "p0", "mu_x", "mu_y", "mu_z")
 N_CHANNELS = 5
 COORD_MODES = ("multiplicative", "additive", "radial")
 BASES = ("gauss", "polyfourier")
+
+
+def _vec3(v, what: str) -> np.ndarray:
+    a = np.asarray(v, dtype=np.float64)
+    if a.shape != (3,):
+        raise ValueError(f"{what} must be a 3-vector")
+    return a
+
+
+@dataclass(frozen=True)
+class Box:
+    """Axis-aligned box [lo, hi] in mm (regions of interest, phantoms)."""
+
+    lo: np.ndarray
+    hi: np.ndarray
+
+    def __post_init__(self):
+        lo, hi = _vec3(self.lo, "lo"), _vec3(self.hi, "hi")
+        if (hi < lo).any():
+            raise ValueError("box hi must be >= lo on every axis")
+        object.__setattr__(self, "lo", lo)
+        object.__setattr__(self, "hi", hi)
+
+    @classmethod
+    def cube(cls, half_extent: float, center=(0.0, 0.0, 0.0)) -> "Box":
+        c = _vec3(center, "center")
+        return cls(c - float(half_extent), c + float(half_extent))
+
+    @property
+    def center(self) -> np.ndarray:
+        return 0.5 * (self.lo + self.hi)
+
+    @property
+    def size(self) -> np.ndarray:
+        return self.hi - self.lo
+
+    def corners(self) -> np.ndarray:
+        bits = (np.arange(8)[:, None] >> np.arange(3)[None, :]) & 1
+        return np.where(bits == 0, self.lo, self.hi)
+
+    def circumradius(self, about=(0.0, 0.0, 0.0)) -> float:
+        """Largest distance from `about` to a corner."""
+        d = self.corners() - _vec3(about, "about")
+        return float(np.sqrt((d * d).sum(axis=1)).max())
+
+    def contains(self, points) -> np.ndarray:
+        """Inclusive test for (n, 3) points."""
+        p = np.atleast_2d(np.asarray(points, dtype=np.float64))
+        return ((p >= self.lo) & (p <= self.hi)).all(axis=1)
+
+
+@dataclass(frozen=True)
+class VoxelGrid:
+    """Regular scalar field; `origin` is the centre of voxel (0, 0, 0)."""
+
+    origin: np.ndarray
+    spacing: float
+    dims: tuple
+    values: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "origin", _vec3(self.origin, "origin"))
+        object.__setattr__(self, "spacing", float(self.spacing))
+        dims = tuple(int(d) for d in self.dims)
+        object.__setattr__(self, "dims", dims)
+        if not self.spacing > 0:
+            raise ValueError("spacing must be > 0")
+        if len(dims) != 3 or min(dims) < 1:
+            raise ValueError("dims must be three integers >= 1")
+        vals = np.ascontiguousarray(self.values, dtype=np.float64)
+        if vals.shape != dims:
+            if vals.size != int(np.prod(dims)):
+                raise ValueError(f"values size {vals.size} != prod(dims) "
+                                 f"{int(np.prod(dims))}")
+            vals = vals.reshape(dims)
+        object.__setattr__(self, "values", vals)
+
+    def voxel_centers_1d(self, axis: int) -> np.ndarray:
+        return self.origin[axis] + self.spacing * np.arange(self.dims[axis])
+
+
+@dataclass(frozen=True)
+class GaussBall:
+    """One spherical Gaussian source (reference core.py:74-101)."""
+
+    p0: float
+    a0: float
+    mu: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "p0", float(self.p0))
+        object.__setattr__(self, "a0", float(self.a0))
+        object.__setattr__(self, "mu", _vec3(self.mu, "mu"))
+        if not self.a0 > 0:
+            raise ValueError(f"a0 must be > 0, got {self.a0}")
+        if self.p0 < 0:
+            raise ValueError(f"p0 must be >= 0, got {self.p0}")
+        if not (np.isfinite(self.p0) and np.isfinite(self.a0)
+                and np.isfinite(self.mu).all()):
+            raise ValueError("ball attributes must be finite")
 
 
 @dataclass(frozen=True)

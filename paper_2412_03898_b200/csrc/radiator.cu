@@ -526,25 +526,60 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     }
 }
 
+static int finish_vec(const void* a, const void* b, const void* c, int T) {
+    const uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                        reinterpret_cast<uintptr_t>(c);
+    return (T % 4 == 0 && (m & 15) == 0) ? 1 : 0;
+}
+
 // Chunk combine (fixed chunk order) + residual + per-trace loss partial.
+// One CTA per (sensor, frame) row; float4 accesses when `vec` (T % 4 == 0
+// and every base pointer 16-byte aligned, checked on the host), scalar
+// otherwise.  HBM-bound: (nchunk + 2) x 4 B/sample.
 // (out may alias partial when nchunk == 1: element-wise, same thread)
-__global__ void __launch_bounds__(256) k_forward_finish(const float* partial,
-                                                        const float* __restrict__ obs,
-                                                        float* out,
-                                                        double* __restrict__ loss, int nchunk,
-                                                        int F, int M, int T) {
+__global__ void __launch_bounds__(256, 4) k_forward_finish(const float* partial,
+                                                           const float* __restrict__ obs,
+                                                           float* out, double* __restrict__ loss,
+                                                           int nchunk, int F, int M, int T,
+                                                           int vec) {
     const int m = blockIdx.x, f = blockIdx.y;
     const size_t row = ((size_t)f * M + m) * T;
     const size_t cstride = (size_t)F * M * T;
     double lsum = 0.0;
-    for (int j = threadIdx.x; j < T; j += blockDim.x) {
-        float s = 0.f;
-        for (int c = 0; c < nchunk; ++c) s += partial[c * cstride + row + j];
-        if (obs) {
-            s -= obs[row + j];
-            lsum = fma((double)s, (double)s, lsum);
+    if (vec) {
+        const int T4 = T >> 2;
+        for (int j = threadIdx.x; j < T4; j += blockDim.x) {
+            float4 s = __ldcs(reinterpret_cast<const float4*>(partial + row) + j);
+            for (int c = 1; c < nchunk; ++c) {
+                const float4 q = __ldcs(reinterpret_cast<const float4*>(partial + c * cstride + row) + j);
+                s.x += q.x;
+                s.y += q.y;
+                s.z += q.z;
+                s.w += q.w;
+            }
+            if (obs) {
+                const float4 o = __ldcs(reinterpret_cast<const float4*>(obs + row) + j);
+                s.x -= o.x;
+                s.y -= o.y;
+                s.z -= o.z;
+                s.w -= o.w;
+                lsum = fma((double)s.x, (double)s.x, lsum);
+                lsum = fma((double)s.y, (double)s.y, lsum);
+                lsum = fma((double)s.z, (double)s.z, lsum);
+                lsum = fma((double)s.w, (double)s.w, lsum);
+            }
+            reinterpret_cast<float4*>(out + row)[j] = s;
         }
-        out[row + j] = s;
+    } else {
+        for (int j = threadIdx.x; j < T; j += blockDim.x) {
+            float s = partial[row + j];
+            for (int c = 1; c < nchunk; ++c) s += partial[c * cstride + row + j];
+            if (obs) {
+                s -= obs[row + j];
+                lsum = fma((double)s, (double)s, lsum);
+            }
+            out[row + j] = s;
+        }
     }
     if (!loss) return;
     __shared__ double red[8];
@@ -895,17 +930,18 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         else
             k_forward<false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         if (p.nchunk > 1) {
-            k_forward_finish<<<dim3(M, F), 256, 0, st>>>(partial, observed, out,
-                                                        want_loss ? lpart : nullptr, p.nchunk,
-                                                        F, M, T);
+            k_forward_finish<<<dim3(M, F), 256, 0, st>>>(
+                partial, observed, out, want_loss ? lpart : nullptr, p.nchunk, F, M, T,
+                finish_vec(partial, observed, out, T));
         }
     } else {
         // empty cloud: zero traces (radiator.py:205-207); residual = -observed
         if (cudaMemsetAsync(out, 0, (size_t)F * M * T * sizeof(float), st) != cudaSuccess)
             return PC_ERR_CUDA;
         if (observed)
-            k_forward_finish<<<dim3(M, F), 256, 0, st>>>(out, observed, out,
-                                                        want_loss ? lpart : nullptr, 1, F, M, T);
+            k_forward_finish<<<dim3(M, F), 256, 0, st>>>(
+                out, observed, out, want_loss ? lpart : nullptr, 1, F, M, T,
+                finish_vec(out, observed, out, T));
     }
     if (want_loss) {
         const int per_frame = (n_balls > 0 && p.nchunk == 1) ? M * p.nseg : M;
@@ -924,7 +960,7 @@ extern "C" int pc_residual_loss(const float* predicted, const float* observed, f
     cudaStream_t st = as_stream(stream);
     k_forward_finish<<<dim3(n_sensors, n_frames), 256, 0, st>>>(
         predicted, observed, out, loss_per_frame ? loss_partial : nullptr, 1, n_frames, n_sensors,
-        n_samples);
+        n_samples, finish_vec(predicted, observed, out, n_samples));
     if (loss_per_frame)
         k_loss_reduce<<<n_frames, 256, 0, st>>>(loss_partial, n_sensors, loss_per_frame);
     return last_status();

@@ -45,6 +45,15 @@ def golden():
     return dict(np.load(GOLDEN))
 
 
+@pytest.fixture(scope="session")
+def pc():
+    """The package with its CUDA library loaded (GPU tests)."""
+    import paper_2412_03898_b200 as pc
+    from paper_2412_03898_b200 import _lib
+    _lib.load_library()
+    return pc
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(1234)

@@ -162,8 +162,93 @@ def main():
     for nm in ("p0", "a0", "mu", "theta", "sigma", "omega"):
         g["dyn_out_" + nm] = getattr(cloud, nm)
 
+    geometry_and_evaluation(g, q32, small)
+    static_stage(g, q32, small)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size / 1024:.0f} KiB, {len(g)} arrays)")
+
+
+def static_stage(g, q32, small):
+    """static_reconstruct on the small sphere array
+    (lattice init, Adam, floors, one prune that drops balls)."""
+    from pacloud.core import Box, ReconConfig
+    from pacloud.deformation import CloudState
+    from pacloud.radiator import forward_frame
+    from pacloud.reconstruction import static_reconstruct
+    rng = np.random.default_rng(77)
+    B = 3
+    st = CloudState(q32(rng.uniform(0.5, 0.9, B)), q32(rng.uniform(0.5, 1, B)),
+                    q32(rng.uniform(-2, 2, (B, 3))))
+    obs = q32(forward_frame(st, small))
+    cfg = ReconConfig(lr_coords=2e-2, lr_pressure=5e-2, lr_std=1e-2,
+                      static_iters=6, prune_every=3, prune_threshold=0.9,
+                      init_pitch=1.5, init_p0_scale=0.5, step_size=4,
+                      drop_rate=0.5, seed=1)
+    roi = Box.cube(2.5)
+    log = []
+    balls = static_reconstruct(obs, small, cfg, roi, progress=log.append)
+    g["static_obs"] = obs
+    g["static_loss"] = np.array([r["loss"] for r in log])
+    g["static_nballs"] = np.array([r["n_balls"] for r in log])
+    g["static_p0"] = np.array([b.p0 for b in balls])
+    g["static_a0"] = np.array([b.a0 for b in balls])
+    g["static_mu"] = np.array([b.mu for b in balls])
+
+
+def geometry_and_evaluation(g, q32, small):
+    """phantoms, arrays, simulate_dataset,
+    voxelize, MAP and SSIM from the live reference."""
+    from pacloud.core import Box
+    from pacloud.deformation import CloudState
+    from pacloud.evaluation import (GridSpec, map_project, normalize_pair,
+                                    ssim, voxelize)
+    from pacloud.geometry import (PhantomSpec, build_phantom,
+                                  fibonacci_sphere, simulate_dataset)
+
+    g["geo_fib"] = fibonacci_sphere(37, 12.5)
+    specs = {
+        "heart": PhantomSpec("heart", Box.cube(12.0), n_frames=3, pitch=1.6,
+                             voxel_pitch=1.0),
+        "vasc": PhantomSpec("vascular", Box.cube(14.0), n_frames=3,
+                            tree_depth=4, seed=3, voxel_pitch=1.0),
+        "custom": PhantomSpec("custom", Box.cube(5.0), n_frames=4,
+                              pulsation=0.2, voxel_pitch=0.5,
+                              custom_balls=((1.0, 0.6, 0.0, 0.0, 0.0),
+                                            (0.5, 0.4, 1.5, -1.0, 2.0))),
+    }
+    for name, spec in specs.items():
+        ph = build_phantom(spec)
+        g[f"ph_{name}_a0"] = np.stack([f.a0_t for f in ph.frames])
+        g[f"ph_{name}_p0"] = np.stack([f.p0_t for f in ph.frames])
+        g[f"ph_{name}_mu"] = np.stack([f.mu_t for f in ph.frames])
+        g[f"ph_{name}_grid0"] = ph.grids[0].values
+        g[f"ph_{name}_gridspec"] = np.concatenate(
+            [ph.grids[0].origin, [ph.grids[0].spacing], ph.grids[0].dims])
+    # simulate_dataset with noise over the custom phantom (small array)
+    ph = build_phantom(specs["custom"])
+    sig = simulate_dataset(ph, small, noise_std=1e-3, seed=7)
+    g["sim_data"] = sig.data
+    # voxelize: a random cloud, fast and exact, odd dims
+    rng = np.random.default_rng(99)
+    B = 40
+    st = CloudState(q32(rng.uniform(0.3, 0.8, B)), q32(rng.uniform(0.2, 1, B)),
+                    q32(rng.uniform(-3, 3, (B, 3))))
+    spec = GridSpec(np.array([-4.0, -3.5, -4.25]), 0.35, (23, 21, 25))
+    g["vox_a0"], g["vox_p0"], g["vox_mu"] = st.a0_t, st.p0_t, st.mu_t
+    g["vox_spec"] = np.concatenate([spec.origin, [spec.spacing], spec.dims])
+    g["vox_fast"] = voxelize(st, spec).values
+    g["vox_exact"] = voxelize(st, spec, exact=True).values
+    # MAP + SSIM between the grid and a perturbed copy
+    st2 = CloudState(st.a0_t * 1.1, st.p0_t, st.mu_t + 0.2)
+    other = voxelize(st2, spec)
+    ss = []
+    for ax in ("XY", "YZ", "XZ"):
+        a, b = normalize_pair(map_project(voxelize(st, spec), ax),
+                              map_project(other, ax))
+        ss.append(ssim(a, b))
+        g[f"map_{ax}"] = map_project(other, ax).values
+    g["ssim_vals"] = np.array(ss)
 
 
 if __name__ == "__main__":

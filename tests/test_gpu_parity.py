@@ -12,14 +12,6 @@ from helpers import GRAD_TOL, SIGNAL_TOL, planar_array, rel_l2, small_array
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def pc():
-    import paper_2412_03898_b200 as pc
-    from paper_2412_03898_b200 import _lib
-    _lib.load_library()
-    return pc
-
-
 def _state(pc, a0, p0, mu):
     return pc.CloudState(np.asarray(a0, float), np.asarray(p0, float),
                          np.asarray(mu, float))
