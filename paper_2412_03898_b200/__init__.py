@@ -12,15 +12,19 @@ include/pacloud_b200.h):
     geometry.simulate_dataset / build_phantom / spherical_array (target
         synthesis on the forward kernel)
     evaluation.voxelize / map_project / ssim / eval_report
+    static.static_reconstruct   single-frame stage (lattice init, prune)
+    fileio.read/write_tensor (PAT1), read/write_cloud (GGB1)
 """
 
 from .core import (AdamState, BallStateAtT, Box, CloudGrads, CloudState,
+                   GaussBall,
                    CloudStateGrad, DynamicCloud, ReconConfig, SensorArray,
                    SignalSet, VoxelGrid, default_basis_grid, frame_times)
 from .deformation import cloud_state_grads, cloud_states_at
 from .engine import IterationEngine
 from .evaluation import (GridSpec, eval_report, format_report, map_project,
                          ssim, voxelize)
+from .fileio import read_cloud, read_tensor, write_cloud, write_tensor
 from .geometry import (Phantom, PhantomSpec, build_phantom, fibonacci_sphere,
                        simulate_dataset, spherical_array)
 from .radiator import (accumulate_frame_grads, forward_frame,
@@ -28,6 +32,7 @@ from .radiator import (accumulate_frame_grads, forward_frame,
 from .reconstruction import (ParamGroup, ParamGroups, adam_step,
                              dynamic_reconstruct, l2_loss, scheduled_lr,
                              sgd_step)
+from .static import static_reconstruct
 
 __version__ = "0.1.0"
 
@@ -41,4 +46,6 @@ __all__ = [
     "Box", "VoxelGrid", "GridSpec", "eval_report", "format_report",
     "map_project", "ssim", "voxelize", "Phantom", "PhantomSpec",
     "build_phantom", "fibonacci_sphere", "simulate_dataset", "spherical_array",
+    "read_cloud", "read_tensor", "write_cloud", "write_tensor",
+    "static_reconstruct", "GaussBall",
 ]

@@ -333,6 +333,12 @@ class DynamicCloud:
     def shared_basis(self) -> bool:
         return self.basis != "gauss" or self.theta.ndim == 2
 
+    @property
+    def balls(self) -> list:
+        """Baseline attributes as GaussBall records (reference core.py:213)."""
+        return [GaussBall(self.p0[i], self.a0[i], self.mu[i])
+                for i in range(len(self))]
+
     @classmethod
     def static(cls, p0, a0, mu, n_basis: int = 1, basis="gauss"):
         """Identity deformation attached to baseline arrays."""

@@ -164,9 +164,38 @@ def main():
 
     geometry_and_evaluation(g, q32, small)
     static_stage(g, q32, small)
+    file_formats(g)
 
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size / 1024:.0f} KiB, {len(g)} arrays)")
+
+
+def file_formats(g):
+    """PAT1 / GGB1 bytes written by the reference."""
+    import tempfile
+    from pacloud.core import DynamicCloud, GaussBall
+    from pacloud.fileio import write_cloud, write_tensor
+    rng = np.random.default_rng(31)
+    t = rng.normal(size=(3, 4, 5))
+    B, N = 4, 3
+    dyn = DynamicCloud(rng.uniform(0.1, 1, B), rng.uniform(0.2, 1, B),
+                       rng.normal(size=(B, 3)), rng.uniform(0, 1, (B, N)),
+                       rng.uniform(0.1, 0.5, (B, N)),
+                       rng.normal(size=(B, 5, N)))
+    balls = [GaussBall(0.5, 0.3, [1.0, 2.0, 3.0]),
+             GaussBall(0.25, 0.7, [-1.5, 0.0, 0.125])]
+    with tempfile.TemporaryDirectory() as d:
+        for name, writer, obj in (("pat", write_tensor, t),
+                                  ("pat0", write_tensor, np.float64(2.5)),
+                                  ("ggb", write_cloud, dyn),
+                                  ("ggb_static", write_cloud, balls)):
+            p = f"{d}/x"
+            writer(p, obj)
+            g[f"file_{name}"] = np.frombuffer(open(p, "rb").read(), np.uint8)
+    g["file_tensor"] = t
+    g["file_dyn_p0"], g["file_dyn_a0"], g["file_dyn_mu"] = dyn.p0, dyn.a0, dyn.mu
+    g["file_dyn_theta"], g["file_dyn_sigma"] = dyn.theta, dyn.sigma
+    g["file_dyn_omega"] = dyn.omega
 
 
 def static_stage(g, q32, small):
