@@ -189,6 +189,24 @@ int pc_voxelize(const double *mu, const double *a0, const double *p0,
                 float *out, int32_t *bad_a0, void *workspace,
                 size_t workspace_bytes, pc_stream_t stream);
 
+/* Replaces reconstruction.py:397-398 (ubp_reconstruct filter):
+ * filtered (M,T) f32 = 2 p - 2 t dp/dt, dp/dt = numpy.gradient along time
+ * (central differences, one-sided ends), t_j = t_start + j / sample_rate;
+ * traces (M,T) f64 on the device. */
+int pc_ubp_filter(const double *traces, int32_t n_sensors, int32_t n_samples,
+                  double t_start, double sample_rate, float *filtered,
+                  pc_stream_t stream);
+
+/* Replaces reconstruction.py:352-377 _backproject: out (nx,ny,nz) f32, C
+ * order, = (1/M) sum_m lerp(filtered_m, (|x - s_m| / v - t_start) / dt) at
+ * voxel centres origin + i*spacing (index truncated, clamped to T-2).
+ * positions (M,3) f64 on the device; origin[3], dims[3] host arrays. */
+int pc_backproject(const float *filtered, const double *positions,
+                   int32_t n_sensors, int32_t n_samples, double sound_speed,
+                   double t_start, double dt, const double *origin,
+                   double spacing, const int32_t *dims, float *out,
+                   pc_stream_t stream);
+
 /* ---- loss and optimiser ------------------------------------------------- */
 
 /* Replaces reconstruction.py:28-35 l2_loss: out[0] = 0.5*sum (p-o)^2 (f64,

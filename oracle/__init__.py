@@ -66,6 +66,10 @@ def _load():
             dp, dp, i64, dp, i64, ctypes.c_double, ctypes.c_double,
             ctypes.c_double, i64, ctypes.c_double, ctypes.c_int, ctypes.c_int]
         lib.oracle_support_samples.restype = i64
+        lib.oracle_backproject.argtypes = [
+            dp, dp, i64, i64, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_double, ctypes.c_double,
+            ctypes.c_double, ctypes.c_double, i64, i64, i64, dp, ctypes.c_int]
         lib.oracle_voxelize.argtypes = [
             dp, dp, dp, i64, ctypes.c_double, ctypes.c_double,
             ctypes.c_double, ctypes.c_double, i64, i64, i64, ctypes.c_double,
@@ -596,3 +600,21 @@ def ssim(a, b, data_range=1.0, window=11, sigma=1.5, k1=0.01, k2=0.03):
     cov = filt(a * b) - ma * mb
     return float(np.mean((2 * ma * mb + c1) * (2 * cov + c2) /
                          ((ma * ma + mb * mb + c1) * (va + vb + c2))))
+
+
+def ubp_reconstruct(traces, array, origin, spacing, dims, threads=0):
+    """reconstruction.py:380-417 (window check omitted): numpy filter
+    b = 2 p - 2 t dp/dt (np.gradient), C restatement of _backproject.
+    Returns (nx, ny, nz) float64."""
+    pos, v, t0, dt, T = _array_fields(array)
+    traces = np.ascontiguousarray(traces, dtype=np.float64)
+    times = array.t_start + np.arange(array.n_samples) / array.sample_rate
+    filt = np.ascontiguousarray(
+        2.0 * traces - 2.0 * times[None, :] * np.gradient(traces, dt, axis=1))
+    dims = tuple(int(d) for d in dims)
+    out = np.zeros(dims)
+    o = np.asarray(origin, dtype=np.float64)
+    _load().oracle_backproject(_dp(filt), _dp(pos), pos.shape[0], T, v, t0,
+                               dt, o[0], o[1], o[2], float(spacing), dims[0],
+                               dims[1], dims[2], _dp(out), int(threads))
+    return out

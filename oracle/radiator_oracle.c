@@ -236,3 +236,45 @@ void oracle_voxelize(const double *mu, const double *a0, const double *p0,
         }
     }
 }
+
+/* reconstruction.py:352-377 _backproject (filtered traces given): out
+ * (nx,ny,nz) = sum_m w * lerp(filtered_m, (|x - s_m| / v - t0) / dt),
+ * w = 1/M, j = int(u) clamped to T - 2. */
+void oracle_backproject(const double *filtered, const double *positions,
+                        int64_t n_sensors, int64_t n_samples, double v,
+                        double t0, double dt, double ox, double oy, double oz,
+                        double sp, int64_t nx, int64_t ny, int64_t nz,
+                        double *out, int n_threads)
+{
+#ifdef _OPENMP
+    if (n_threads > 0) omp_set_num_threads(n_threads);
+#else
+    (void)n_threads;
+#endif
+    const double w = 1.0 / (double)n_sensors;
+    int64_t ix;
+#pragma omp parallel for schedule(static)
+    for (ix = 0; ix < nx; ++ix) {
+        const double x = ox + ix * sp;
+        for (int64_t iy = 0; iy < ny; ++iy) {
+            const double y = oy + iy * sp;
+            for (int64_t iz = 0; iz < nz; ++iz) {
+                const double z = oz + iz * sp;
+                double acc = 0.0;
+                for (int64_t m = 0; m < n_sensors; ++m) {
+                    const double dx = x - positions[3 * m];
+                    const double dy = y - positions[3 * m + 1];
+                    const double dz = z - positions[3 * m + 2];
+                    const double tof = sqrt(dx * dx + dy * dy + dz * dz) / v;
+                    const double u = (tof - t0) / dt;
+                    int64_t j = (int64_t)u;
+                    if (j >= n_samples - 1) j = n_samples - 2;
+                    const double fr = u - (double)j;
+                    const double *f = filtered + m * n_samples;
+                    acc += w * ((1.0 - fr) * f[j] + fr * f[j + 1]);
+                }
+                out[(ix * ny + iy) * nz + iz] = acc;
+            }
+        }
+    }
+}

@@ -14,6 +14,7 @@ include/pacloud_b200.h):
     evaluation.voxelize / map_project / ssim / eval_report
     static.static_reconstruct   single-frame stage (lattice init, prune)
     fileio.read/write_tensor (PAT1), read/write_cloud (GGB1)
+    ubp.ubp_reconstruct         universal back-projection comparator
 """
 
 from .core import (AdamState, BallStateAtT, Box, CloudGrads, CloudState,
@@ -33,6 +34,7 @@ from .reconstruction import (ParamGroup, ParamGroups, adam_step,
                              dynamic_reconstruct, l2_loss, scheduled_lr,
                              sgd_step)
 from .static import static_reconstruct
+from .ubp import ubp_reconstruct
 
 __version__ = "0.1.0"
 
@@ -47,5 +49,5 @@ __all__ = [
     "map_project", "ssim", "voxelize", "Phantom", "PhantomSpec",
     "build_phantom", "fibonacci_sphere", "simulate_dataset", "spherical_array",
     "read_cloud", "read_tensor", "write_cloud", "write_tensor",
-    "static_reconstruct", "GaussBall",
+    "static_reconstruct", "GaussBall", "ubp_reconstruct",
 ]

@@ -187,6 +187,26 @@ def raise_if_coincident(coincident, mu_t, positions):
                      f"(distance {d:.3g} mm)")
 
 
+def compute_time_window(array, roi, margin_a0: float):
+    """radiator.py:297-322: (t_start, n_samples) covering time of flight to
+    the nearest / farthest ROI points (circumscribed about the origin),
+    padded by 6 margin_a0 on each side, count rounded up."""
+    if margin_a0 < 0:
+        raise ValueError("margin_a0 must be >= 0")
+    norms = np.linalg.norm(np.asarray(array.positions, float), axis=1)
+    r_near, r_far = float(norms.min()), float(norms.max())
+    r_roi = roi.circumradius()
+    if r_roi >= r_near:
+        raise ValueError(
+            f"roi circumscribed radius {r_roi:.3f} mm reaches the sensor "
+            f"sphere (nearest sensor at {r_near:.3f} mm)")
+    pad = 6.0 * margin_a0
+    t_lo = max(0.0, (r_near - r_roi - pad) / array.sound_speed)
+    t_hi = (r_far + r_roi + pad) / array.sound_speed
+    span = max(0.0, (t_hi - t_lo) * array.sample_rate - 1e-9)
+    return t_lo, int(np.ceil(span)) + 1
+
+
 # ---------------------------------------------------------------- drop-ins
 
 def _as_cloud_state(states):

@@ -165,9 +165,36 @@ def main():
     geometry_and_evaluation(g, q32, small)
     static_stage(g, q32, small)
     file_formats(g)
+    ubp_golden(g, q32)
 
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size / 1024:.0f} KiB, {len(g)} arrays)")
+
+
+def ubp_golden(g, q32):
+    """ubp_reconstruct of a simulated frame."""
+    from pacloud.core import Box
+    from pacloud.deformation import CloudState
+    from pacloud.evaluation import GridSpec
+    from pacloud.geometry import spherical_array
+    from pacloud.radiator import compute_time_window, forward_frame
+    from pacloud.reconstruction import ubp_reconstruct
+    rng = np.random.default_rng(55)
+    roi = Box.cube(4.0)
+    arr = spherical_array(48, 25.0, sample_rate=8.0)
+    t0, n = compute_time_window(arr, roi, 1.0)
+    arr = arr.with_window(t0, n)
+    B = 6
+    st = CloudState(q32(rng.uniform(0.4, 0.9, B)), q32(rng.uniform(0.3, 1, B)),
+                    q32(rng.uniform(-2.5, 2.5, (B, 3))))
+    tr = q32(forward_frame(st, arr))
+    spec = GridSpec.from_box(roi, 0.5)
+    g["ubp_pos"] = arr.positions
+    g["ubp_cfg"] = np.array([arr.sound_speed, arr.sample_rate, arr.n_samples,
+                             arr.t_start])
+    g["ubp_traces"] = tr
+    g["ubp_spec"] = np.concatenate([spec.origin, [spec.spacing], spec.dims])
+    g["ubp_grid"] = ubp_reconstruct(tr, arr, spec).values
 
 
 def file_formats(g):
