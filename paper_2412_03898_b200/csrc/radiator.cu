@@ -192,8 +192,9 @@ struct FwdArgs {
 // Gaussian term of one sample pair: x 2^(-x^2)
 __device__ __forceinline__ float2 gterm(float2 x) { return fmul2(x, ex2n_2(fmul2(x, x))); }
 
-// Record word 0: je0 | span << 15 | near << 30 | recur << 31 (span = je1 - je0,
-// even; recur: the ball's Gaussian may be stepped by recurrence, recur_ok).
+// Record word 0: je0 | span << 15 | slow << 30 | recur << 31 (span = je1 - je0,
+// even; per ball: slow = a pair of the ball needs the near field (or exact),
+// recur = the Gaussian may be stepped by recurrence, recur_ok).
 __device__ __forceinline__ int rec_je0(int w) { return w & 0x7fff; }
 __device__ __forceinline__ int rec_span(int w) { return (w >> 15) & 0x7fff; }
 
@@ -248,19 +249,21 @@ __device__ __forceinline__ void fwd_sweep_fast(float2* __restrict__ trl, float4 
 // Fast path by recurrence (the adjoint's scheme): with D = FSTR s v dt,
 // e = 2^-x^2 steps as e <- e g, g <- g h (g = 2^(2 D x - D^2), h = 2^(-2 D^2)),
 // so MUFU runs only at the lane's first sample.  Same lane layout as
-// fwd_sweep_fast; r0.w = dx = -D, h from the record.
-__device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4 r0, float h,
+// fwd_sweep_fast (r0.w = dx = -D); r1 = {2D, -D^2, h, nfull | tail << 16}
+// from the setup pass: nfull steps are live on every lane of the half, one
+// more where 2 sub < tail.
+__device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4 r0, float4 r1,
                                                 int sub2i, float2 subq) {
     const int w = __float_as_int(r0.x);
-    const int span = rec_span(w);
+    const int nr = __float_as_int(r1.w);
     const float2 dx = splat2(r0.w);
     const float2 cc = splat2(r0.z);
     float2 x = ffma2(subq, dx, splat2(r0.y));
     float2 e = ex2n_2(fmul2(x, x));
-    float2 g = ex2_2(ffma2(x, splat2(-2.f * r0.w), splat2(-r0.w * r0.w)));
-    const float2 h2 = splat2(h);
+    float2 g = ex2_2(ffma2(x, splat2(r1.x), splat2(r1.y)));
+    const float2 h2 = splat2(r1.z);
     float2* p = trl + (rec_je0(w) >> 1);
-    const int nfull = (span + 1) / FSTR;
+    const int nfull = nr & 0xffff;
     int n = nfull;
 #define PC_FWD_RSTEP(V)   \
     V = fmul2(x, e);      \
@@ -296,7 +299,7 @@ __device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4
         p += FL;
     }
 #undef PC_FWD_RSTEP
-    if (sub2i + nfull * FSTR < span) *p = ffma2(cc, fmul2(x, e), *p);
+    if (sub2i < (nr >> 16)) *p = ffma2(cc, fmul2(x, e), *p);
 }
 
 // Exact window / near field: x (and y) from the exact integer offset to the
@@ -306,7 +309,7 @@ __device__ __forceinline__ void fwd_sweep_slow(float2* __restrict__ trl, float4 
                                                float2 sub2, int sub2i) {
     const int w = __float_as_int(r0.x);
     const int je0 = rec_je0(w);
-    const bool near = (w >> 30) & 1;
+    const bool near = (w >> 30) & 1;        // the ball's slow flag: evaluate the near field
     const int nl = (rec_span(w) - sub2i + FSTR - 1) / FSTR;
     const float vs = r0.w * (-1.f / FSTR);
     const float2 cc = splat2(r0.z);
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 const float w = sup * cur.w + 1e-5f * r;
                 pass = EXACT || r < 1e-3f || (r + w >= d_lo && r - w <= d_hi);
             }
-            float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+            float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0, qr = q0;
             bool slow = false;
             if (pass) {
                 const float av = cur.w;
@@ -452,19 +455,34 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     const int je0 = q.jl & ~1;
                     const int je1 = (q.jh + 1) & ~1;
                     const float X0 = fmaf((float)(q.jr - je0), vs, q.X);
-                    q0 = make_float4(
-                        __int_as_float(je0 | ((je1 - je0) << 15) | (q.near ? 1 << 30 : 0)), X0, c,
-                        -(float)FSTR * vs);
                     const float D = (float)FSTR * vs;
-                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), ex2(-2.f * D * D));
+                    q0 = make_float4(__int_as_float(je0 | ((je1 - je0) << 15)), X0, c, -D);
+                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), 0.f);
+                    const int nfull = (je1 - je0 + 1) / FSTR;
+                    qr = make_float4(2.f * D, -D * D, ex2(-2.f * D * D),
+                                     __int_as_float(nfull | ((je1 - je0 - nfull * FSTR) << 16)));
                     slow = EXACT || q.near;
                 }
             }
-            if (!EXACT) {
-                // per ball (both sensors of the warp agree): recurrence stepping
-                const float vsb = vdt * scale_of(cur.w);
-                if (recur_ok((float)FSTR * vsb, vsb, sup))
-                    q0.x = __int_as_float(__float_as_int(q0.x) | (int)0x80000000u);
+            {
+                // per ball (both sensors of the warp agree): the direct form
+                // when either pair needs the near field (bit 30, record 1 =
+                // {X, Y, jr}), else the recurrence when its bounds hold
+                // (bit 31, record 1 = {2D, -D^2, h, nfull | tail << 16})
+                // (the shuffle must run on every lane: no short-circuit)
+                const bool pslow = __shfl_xor_sync(0xffffffffu, slow, FL);
+                const bool bslow = slow || pslow;
+                int w = __float_as_int(q0.x);
+                if (bslow) {
+                    w |= 1 << 30;
+                } else if (!EXACT) {
+                    const float vsb = vdt * scale_of(cur.w);
+                    if (recur_ok((float)FSTR * vsb, vsb, sup)) {
+                        w |= (int)0x80000000u;
+                        q1 = qr;
+                    }
+                }
+                q0.x = __int_as_float(w);
             }
             // compact: balls with a live pair for either sensor, in batch order
             const unsigned pm = __ballot_sync(0xffffffffu, pass);
@@ -479,16 +497,11 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             __syncwarp();
             for (int k = 0; k < nb; ++k) {
                 const float4 r0 = recs[k].r0;
-                const bool rec = __float_as_int(r0.x) < 0;
-                bool sl = false;
-                if (anyslow) {
-                    sl = EXACT || ((__float_as_int(r0.x) >> 30) & 1);
-                    sl = __any_sync(0xffffffffu, sl);
-                }
-                if (sl)
+                const int w = __float_as_int(r0.x);
+                if (w < 0)
+                    fwd_sweep_recur(trl, r0, recs[k].r1, 2 * sub, subq);
+                else if (EXACT || (anyslow && ((w >> 30) & 1)))
                     fwd_sweep_slow(trl, r0, recs[k].r1, sub2, 2 * sub);
-                else if (rec)
-                    fwd_sweep_recur(trl, r0, recs[k].r1.w, 2 * sub, subq);
                 else
                     fwd_sweep_fast(trl, r0, 2 * sub, subq);
                 __syncwarp();
