@@ -784,9 +784,19 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
                             PC_ADJ_STEP(rr[u])
                         }
                     }
-                    for (; n > 0; --n, j += LSTRIDE) {
-                        const float4 r = load_quad<ALIGNED>(row, j, T);
-                        PC_ADJ_STEP(r)
+                    if (n > 0) {
+                        // remainder (< 4 quads): all loads in flight at once
+                        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 r0q = load_quad<ALIGNED>(row, j, T);
+                        const float4 r1q = n > 1 ? load_quad<ALIGNED>(row, j + LSTRIDE, T) : z;
+                        const float4 r2q = n > 2 ? load_quad<ALIGNED>(row, j + 2 * LSTRIDE, T) : z;
+                        PC_ADJ_STEP(r0q)
+                        if (n > 1) {
+                            PC_ADJ_STEP(r1q)
+                        }
+                        if (n > 2) {
+                            PC_ADJ_STEP(r2q)
+                        }
                     }
 #undef PC_ADJ_STEP
                 } else {
