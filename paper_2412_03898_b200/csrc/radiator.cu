@@ -642,6 +642,11 @@ constexpr int ADJ_WARPS = 4;      // balls per CTA
 constexpr int LG = 4;             // lanes per pair (adjoint)
 constexpr int NGRP = 32 / LG;     // pairs in flight per warp
 constexpr int LSTRIDE = 4 * LG;   // samples between a lane's successive quads
+// Gaussian per chain in the sweep: 0 = both chains by recurrence, 1 = chain a
+// by MUFU and chain b by recurrence, 2 = both by MUFU.
+#ifndef PC_ADJ_MODE
+#define PC_ADJ_MODE 2
+#endif
 
 struct AdjArgs {
     const double* mu;
@@ -675,6 +680,20 @@ __device__ __forceinline__ void accum_pair(float2 r, float2 e, float2 x, float2&
     const float2 t = fmul2(w, x);
     A1 = fadd2(A1, t);
     const float2 u = fmul2(t, x);
+    A2 = fadd2(A2, u);
+    A3 = ffma2(u, x, A3);
+}
+
+// The same moments with e = 2^-x^2 from MUFU: x^2 is then at hand for the
+// second moment, 6 packed FMA-pipe ops + 2 MUFU per sample pair (against 7
+// + the recurrence's 2), moving work from the FMA pipe to the idle XU pipe.
+__device__ __forceinline__ void accum_pair_mufu(float2 r, float2 x, float2& A0, float2& A1,
+                                                float2& A2, float2& A3) {
+    const float2 xx = fmul2(x, x);
+    const float2 w = fmul2(r, ex2n_2(xx));
+    A0 = fadd2(A0, w);
+    A1 = ffma2(w, x, A1);
+    const float2 u = fmul2(w, xx);
     A2 = fadd2(A2, u);
     A3 = ffma2(u, x, A3);
 }
@@ -765,6 +784,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
                     recur_init(xa, D, ea, ga);
                     recur_init(xb, D, eb, gb);
                     int n = (je1 - j + LSTRIDE - 1) / LSTRIDE;   // quads of this lane
+#if PC_ADJ_MODE == 0
 #define PC_ADJ_STEP(R)                                   \
     accum_pair(lo2(R), ea, xa, A0, A1, A2, A3);          \
     accum_pair(hi2(R), eb, xb, A0, A1, A2, A3);          \
@@ -774,6 +794,21 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     gb = fmul2(gb, h2);                                  \
     xa = fadd2(xa, mD2);                                 \
     xb = fadd2(xb, mD2);
+#elif PC_ADJ_MODE == 1
+#define PC_ADJ_STEP(R)                                   \
+    accum_pair_mufu(lo2(R), xa, A0, A1, A2, A3);         \
+    accum_pair(hi2(R), eb, xb, A0, A1, A2, A3);          \
+    eb = fmul2(eb, gb);                                  \
+    gb = fmul2(gb, h2);                                  \
+    xa = fadd2(xa, mD2);                                 \
+    xb = fadd2(xb, mD2);
+#else
+#define PC_ADJ_STEP(R)                                   \
+    accum_pair_mufu(lo2(R), xa, A0, A1, A2, A3);         \
+    accum_pair_mufu(hi2(R), xb, A0, A1, A2, A3);         \
+    xa = fadd2(xa, mD2);                                 \
+    xb = fadd2(xb, mD2);
+#endif
                     // chunks of 4 quads: 4 independent loads in flight
                     for (; n >= 4; n -= 4, j += 4 * LSTRIDE) {
                         float4 rr[4];
