@@ -28,6 +28,7 @@ rank, i.e. broadcast).  Both end in the same gradient all-reduce.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -194,6 +195,9 @@ class IterationEngine:
                                       device=self.device)
         self.host_observed = None
         self._copy_stream = None
+        # frame groups for forward / adjoint overlap (PC_FRAME_GROUPS)
+        self.frame_groups = int(os.environ.get("PC_FRAME_GROUPS", "1"))
+        self._adj_stream = None
 
     def stream_observed_from(self, host):
         """Upload the observed traces from pinned host memory every iteration
@@ -259,22 +263,48 @@ class IterationEngine:
         deform_states_device(self.dcloud, self.t_dev, cfg.coord_mode,
                              cfg.a0_floor, self.mu_t, self.a0_t, self.p0_t,
                              self.H)
-        if host_src is None:
-            forward_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
-                           observed=obs, out=self.resid, loss=self.loss_f,
-                           coincident=self.coinc, workspace=self.ws)
-        else:
-            forward_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
-                           observed=None, out=self.resid,
-                           coincident=self.coinc, workspace=self.ws)
-            cur.wait_stream(self._copy_stream)
-            residual_loss_device(self.resid, obs, out=self.resid,
-                                 loss=self.loss_f, partial=self.loss_part)
-        state_grads_device(self.darr, self.mu_t, self.a0_t, self.p0_t,
-                           self.resid, G=self.G, coincident=self.coinc)
+        F = int(self.mu_t.shape[0])
+        groups = self._frame_groups(F)
+        adj = cur if len(groups) == 1 else self._adj_stream
+        waited_copy = False
+        for f0, f1 in groups:
+            mu, a0, p0 = self.mu_t[f0:f1], self.a0_t[f0:f1], self.p0_t[f0:f1]
+            res, loss = self.resid[f0:f1], self.loss_f[f0:f1]
+            if host_src is None:
+                forward_device(self.darr, mu, a0, p0, observed=obs[f0:f1],
+                               out=res, loss=loss, coincident=self.coinc,
+                               workspace=self.ws)
+            else:
+                forward_device(self.darr, mu, a0, p0, observed=None, out=res,
+                               coincident=self.coinc, workspace=self.ws)
+                if not waited_copy:
+                    cur.wait_stream(self._copy_stream)
+                    waited_copy = True
+                residual_loss_device(res, obs[f0:f1], out=res, loss=loss,
+                                     partial=self.loss_part[f0 * self.darr.M:])
+            if adj is not cur:
+                # this group's adjoint overlaps the next group's forward
+                adj.wait_stream(cur)
+            with torch.cuda.stream(adj):
+                state_grads_device(self.darr, mu, a0, p0, res,
+                                   G=self.G[f0:f1], coincident=self.coinc)
+        if adj is not cur:
+            cur.wait_stream(adj)
         deform_backward_device(self.dcloud, self.t_dev, cfg.coord_mode,
                                cfg.a0_floor, self.G, self.H, self.grads)
         torch.sum(self.loss_f, dim=0, keepdim=True, out=self.loss_total)
+
+    def _frame_groups(self, F: int):
+        """Frame groups of the iteration: forward of group g+1 runs while
+        the adjoint of group g runs on a second stream (the kernels are
+        limited by different resources: shared memory / issue for the
+        forward, registers / FMA + XU pipes for the adjoint)."""
+        n = max(1, min(int(self.frame_groups), F))
+        if n > 1 and self._adj_stream is None:
+            self._adj_stream = torch.cuda.Stream(device=self.device)
+        bounds = np.linspace(0, F, n + 1).round().astype(int)
+        return [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:])
+                if b > a]
 
     def compute_grads(self, frames: np.ndarray) -> None:
         """Launch (asynchronously) the gradient of the selected frames."""
