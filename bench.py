@@ -238,7 +238,7 @@ def run_reference(args, rank, world):
 
 def workload_config(cfg_id, prob, world):
     shp = prob.meta["shape"]
-    shard = "sensors" if cfg_id == 4 else "frames"
+    shard = "sensors" if (cfg_id == 4 or shp["F"] < world) else "frames"
     return {"workload": f"BASELINE config {cfg_id}",
             "balls": shp["B"], "sensors": shp["M"], "samples": shp["T"],
             "frames": shp["F"], "basis": prob.cloud.basis,
@@ -256,12 +256,18 @@ def run_ours(args, rank, world, local):
     from paper_2412_03898_b200.engine import IterationEngine
     from paper_2412_03898_b200.radiator import DeviceArray, forward_device
 
+    # one process per GPU; PC_DIST_BACKEND=gloo with more ranks than GPUs is
+    # a functional check of the sharded path only (never a measurement)
+    backend = os.environ.get("PC_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" \
+        else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import datetime
+        kw = {"device_id": dev} if backend == "nccl" else {}
         torch.distributed.init_process_group(
-            "nccl", device_id=dev, timeout=datetime.timedelta(minutes=10))
+            backend, timeout=datetime.timedelta(minutes=10), **kw)
     prob = synth.make_problem(args.config, seed=args.seed)
     shp = prob.meta["shape"]
     B, M, T, F = shp["B"], shp["M"], shp["T"], shp["F"]
@@ -280,7 +286,9 @@ def run_ours(args, rank, world, local):
         obs[k] = o[0]
     del darr_full
 
-    sensor_shard = args.config == 4 and world > 1
+    # sensors are sharded for config 4 and whenever the frames cannot cover
+    # the ranks (config 1 has one frame)
+    sensor_shard = world > 1 and (args.config == 4 or F < world)
     frames_all = np.arange(F)
     if sensor_shard:
         lo, hi = shard_range(M, rank, world)
