@@ -57,6 +57,20 @@ static int fwd_tseg_max() {
 
 static size_t fwd_smem_bytes(int Tseg);
 
+// Target waves of resident CTAs when balls are chunked (PC_FWD_WAVES; 8
+// measured best on config 2: 2 / 4 / 6 / 8 / 12 waves -> 7.39 / 7.07 / 6.91 /
+// 6.72 / 6.71 ms, finer ball chunks balance the CTAs and keep each chunk's
+// ball data cache-resident).
+static int fwd_waves() {
+    static int v = 0;
+    if (v == 0) {
+        const char* e = getenv("PC_FWD_WAVES");
+        const int x = e ? atoi(e) : 0;
+        v = (x >= 1 && x <= 16) ? x : 8;
+    }
+    return v;
+}
+
 static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     FwdPlan p;
     const int tmax = fwd_tseg_max();
@@ -67,7 +81,8 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     // ask for >= 2 waves of resident CTAs so the tail stays short
     const int64_t base = tiles * F * (p.nseg > 1 ? p.nseg / 2 : 1);
     const int per_sm = (int)(228 * 1024 / (fwd_smem_bytes(p.Tseg) + 1024));
-    const int64_t want = 2LL * (per_sm < 1 ? 1 : per_sm > 16 ? 16 : per_sm) * num_sms();
+    const int64_t want = (int64_t)fwd_waves() * (per_sm < 1 ? 1 : per_sm > 16 ? 16 : per_sm) *
+                         num_sms();
     int64_t c = base >= want ? 1 : (want + base - 1) / base;
     const int64_t cmax = B / 256 > 1 ? B / 256 : 1;
     if (c > cmax) c = cmax;
