@@ -35,7 +35,7 @@ constexpr int FSW = 2;              // sensors per warp (16 lanes each)
 constexpr int FL = 32 / FSW;        // lanes per (ball, sensor) pair
 constexpr int FSTR = 2 * FL;        // samples between a lane's successive pairs
 constexpr int FBATCH = 32 / FSW;    // balls per setup batch (one lane per pair)
-constexpr int FWD_TSEG_MAX = 1536;  // samples per time segment (private traces)
+constexpr int FWD_TSEG_MAX = 1024;  // samples per time segment (private traces)
 constexpr int TRACE_PAD = 8;        // floats after a trace (even-window overrun)
 
 struct FwdPlan {
@@ -57,16 +57,16 @@ static int fwd_tseg_max() {
 
 static size_t fwd_smem_bytes(int Tseg);
 
-// Target waves of resident CTAs when balls are chunked (PC_FWD_WAVES; 8
-// measured best on config 2: 2 / 4 / 6 / 8 / 12 waves -> 7.39 / 7.07 / 6.91 /
-// 6.72 / 6.71 ms, finer ball chunks balance the CTAs and keep each chunk's
-// ball data cache-resident).
+// Target waves of resident CTAs when balls are chunked (PC_FWD_WAVES).  With
+// per-(frame, chunk) bounding boxes, finer Morton chunks also tighten each
+// warp's arrival range; measured on config 2 (segment cap 1024): 8 / 12 / 20
+// / 32 waves -> 5.84 / 5.49 / 5.47 / 5.52 ms forward.
 static int fwd_waves() {
     static int v = 0;
     if (v == 0) {
         const char* e = getenv("PC_FWD_WAVES");
         const int x = e ? atoi(e) : 0;
-        v = (x >= 1 && x <= 16) ? x : 8;
+        v = (x >= 1 && x <= 64) ? x : 12;
     }
     return v;
 }
@@ -92,9 +92,9 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     p.partial_bytes = p.nchunk > 1 ? (size_t)p.nchunk * F * M * T * sizeof(float) : 0;
     const int nloss = p.nchunk > 1 ? 1 : p.nseg;
     p.loss_bytes = (size_t)F * M * nloss * sizeof(double);
-    // cull records (F,B) float4 + per-frame bounds (8 u32), 256-byte aligned
+    // cull records (F,B) float4 + per-(frame, chunk) bounds (8 u32), 256-byte aligned
     p.prep_bytes = (((size_t)F * B * sizeof(float4) + 255) / 256) * 256 +
-                   (size_t)F * 8 * sizeof(unsigned);
+                   (size_t)F * p.nchunk * 8 * sizeof(unsigned);
     return p;
 }
 
@@ -123,12 +123,19 @@ __device__ __forceinline__ float ord2f(unsigned u) {
 // (min xyz, max xyz as ~code, max a0 as ~code: all atomicMin, init 0xff..).
 __global__ void __launch_bounds__(256) k_forward_prep(const double* __restrict__ mu,
                                                       const float* __restrict__ a0, int64_t B,
-                                                      int F, float4* __restrict__ cull,
+                                                      int F, int nchunk, int64_t chunk_balls,
+                                                      int bpc, float4* __restrict__ cull,
                                                       unsigned* __restrict__ bounds) {
+    // blockIdx.x = chunk * bpc + block within the chunk: bounds per (frame,
+    // ball chunk), so a chunk's warps lay their traces over the arrival
+    // range of that chunk's balls only
     const int f = blockIdx.y;
+    const int c = blockIdx.x / bpc;
+    const int64_t c0 = (int64_t)c * chunk_balls;
+    const int64_t c1 = min(B, c0 + chunk_balls);
     unsigned mn[3] = {~0u, ~0u, ~0u}, mxn[4] = {~0u, ~0u, ~0u, ~0u};
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < B;
-         b += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t b = c0 + (int64_t)(blockIdx.x % bpc) * blockDim.x + threadIdx.x; b < c1;
+         b += (int64_t)bpc * blockDim.x) {
         const size_t s = (size_t)f * B + b;
         const float x = (float)mu[3 * s], y = (float)mu[3 * s + 1], z = (float)mu[3 * s + 2];
         const float a = a0[s];
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(256) k_forward_prep(const double* __restrict__
         mxn[3] = min(mxn[3], __shfl_xor_sync(0xffffffffu, mxn[3], o));
     }
     if ((threadIdx.x & 31) == 0) {
-        unsigned* bf = bounds + 8 * f;
+        unsigned* bf = bounds + 8 * ((size_t)f * nchunk + c);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             atomicMin(bf + k, mn[k]);
@@ -382,7 +389,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     int act_lo = 0, act_hi = T;
     float dmin_box = 0.f;
     if (!EXACT) {
-        const unsigned* bf = a.bounds + 8 * f;
+        const unsigned* bf = a.bounds + 8 * ((size_t)f * a.nchunk + chunk);
         const float lx = ord2f(bf[0]), ly = ord2f(bf[1]), lz = ord2f(bf[2]);
         const float hx = ord2f(~bf[3]), hy = ord2f(~bf[4]), hz = ord2f(~bf[5]);
         const float amax = ord2f(~bf[6]);
@@ -964,12 +971,15 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
     const bool want_loss = observed && loss_per_frame;
 
     if (n_balls > 0) {
-        if (cudaMemsetAsync(bounds, 0xff, (size_t)F * 8 * sizeof(unsigned), st) != cudaSuccess)
+        if (cudaMemsetAsync(bounds, 0xff, (size_t)F * p.nchunk * 8 * sizeof(unsigned), st) !=
+            cudaSuccess)
             return PC_ERR_CUDA;
-        int64_t pb = (n_balls + 255) / 256;
-        if (pb > 2LL * num_sms()) pb = 2LL * num_sms();
-        k_forward_prep<<<dim3((unsigned)pb, F), 256, 0, st>>>(mu_t, a0_t, n_balls, F, cull,
-                                                              bounds);
+        int64_t bpc = (p.chunk_balls + 255) / 256;      // prep blocks per chunk
+        const int64_t cap = (2LL * num_sms() + p.nchunk - 1) / p.nchunk;
+        if (bpc > cap) bpc = cap;
+        if (bpc < 1) bpc = 1;
+        k_forward_prep<<<dim3((unsigned)(bpc * p.nchunk), F), 256, 0, st>>>(
+            mu_t, a0_t, n_balls, F, p.nchunk, p.chunk_balls, (int)bpc, cull, bounds);
         FwdArgs a;
         a.mu = mu_t;
         a.p0 = p0_t;
