@@ -674,7 +674,10 @@ __global__ void __launch_bounds__(256) k_loss_reduce(const double* __restrict__ 
 // warp reduces once per ball (fixed xor order: deterministic).
 
 constexpr int ADJ_WARPS = 4;      // balls per CTA
-constexpr int LG = 4;             // lanes per pair (adjoint)
+#ifndef PC_ADJ_LG
+#define PC_ADJ_LG 2
+#endif
+constexpr int LG = PC_ADJ_LG;             // lanes per pair (adjoint; 1 / 2 / 4 / 8 -> 6.16 / 5.12 / 5.53 / 7.08 ms on config 2)
 constexpr int NGRP = 32 / LG;     // pairs in flight per warp
 constexpr int LSTRIDE = 4 * LG;   // samples between a lane's successive quads
 // Gaussian per chain in the sweep: 0 = both chains by recurrence, 1 = chain a
