@@ -184,6 +184,7 @@ class IterationEngine:
         self.dcloud = DeviceCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
                                   p.get("sigma"), p["omega"], self.basis)
         self.use_graph = bool(use_graph)
+        self._warmed = False
         self._graph = None
         self._graph_frames = None
         self._bufs_F = -1
@@ -343,9 +344,13 @@ class IterationEngine:
         self.t_dev.copy_(torch.as_tensor(self.frame_times_all[local],
                                          dtype=torch.float64))
         if self.use_graph and contiguous:
-            # warm once eagerly (lazy init inside torch / the driver), then
-            # capture the fixed launch sequence and replay it from now on
-            self._launch_compute(obs, host_src)
+            # warm once eagerly per engine (lazy init inside torch / the
+            # driver / the library's function attributes), then capture the
+            # fixed launch sequence and replay it from now on; re-captures
+            # after a change of frames or ball count skip the warm-up
+            if not self._warmed:
+                self._launch_compute(obs, host_src)
+                self._warmed = True
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream())
