@@ -673,13 +673,20 @@ __global__ void __launch_bounds__(256) k_loss_reduce(const double* __restrict__ 
 // deferred: lanes fold their partials into five ball accumulators and the
 // warp reduces once per ball (fixed xor order: deterministic).
 
-constexpr int ADJ_WARPS = 4;      // balls per CTA
+#ifndef PC_ADJ_WARPS
+#define PC_ADJ_WARPS 4
+#endif
+constexpr int ADJ_WARPS = PC_ADJ_WARPS;   // balls per CTA
 #ifndef PC_ADJ_LG
 #define PC_ADJ_LG 2
 #endif
 constexpr int LG = PC_ADJ_LG;             // lanes per pair (adjoint; 1 / 2 / 4 / 8 -> 6.16 / 5.12 / 5.53 / 7.08 ms on config 2)
 constexpr int NGRP = 32 / LG;     // pairs in flight per warp
 constexpr int LSTRIDE = 4 * LG;   // samples between a lane's successive quads
+#ifndef PC_ADJ_CHUNK
+#define PC_ADJ_CHUNK 4
+#endif
+constexpr int ADJ_CHUNK = PC_ADJ_CHUNK;   // residual quads loaded per wave
 // Gaussian per chain in the sweep: 0 = both chains by recurrence, 1 = chain a
 // by MUFU and chain b by recurrence, 2 = both by MUFU.
 #ifndef PC_ADJ_MODE
@@ -847,8 +854,18 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     xa = fadd2(xa, mD2);                                 \
     xb = fadd2(xb, mD2);
 #endif
-                    // chunks of 4 quads: 4 independent loads in flight
-                    for (; n >= 4; n -= 4, j += 4 * LSTRIDE) {
+                    // chunks of ADJ_CHUNK quads: that many loads in flight
+                    for (; n >= ADJ_CHUNK; n -= ADJ_CHUNK, j += ADJ_CHUNK * LSTRIDE) {
+                        float4 rr[ADJ_CHUNK];
+#pragma unroll
+                        for (int u = 0; u < ADJ_CHUNK; ++u)
+                            rr[u] = load_quad<ALIGNED>(row, j + u * LSTRIDE, T);
+#pragma unroll
+                        for (int u = 0; u < ADJ_CHUNK; ++u) {
+                            PC_ADJ_STEP(rr[u])
+                        }
+                    }
+                    if (ADJ_CHUNK > 4 && n >= 4) {
                         float4 rr[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) rr[u] = load_quad<ALIGNED>(row, j + u * LSTRIDE, T);
@@ -856,6 +873,8 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
                         for (int u = 0; u < 4; ++u) {
                             PC_ADJ_STEP(rr[u])
                         }
+                        n -= 4;
+                        j += 4 * LSTRIDE;
                     }
                     if (n > 0) {
                         // remainder (< 4 quads): all loads in flight at once
