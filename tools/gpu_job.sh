@@ -15,4 +15,10 @@ CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 60 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_forward$|k_adjoint" -s 8 -c 2 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full.log 2>&1
+# every kernel of one config-2 iteration (one launch each) and the config-5
+# densify / compaction kernels
+timeout 1200 ncu --set full --clock-control none -k regex:"^k_" -s 40 -c 12 -o gpurun_out/prof_${TAG}_all $CMD > gpurun_out/ncu_all.log 2>&1
+C5="python bench.py --config 5 --steps 1 --warmup 3 --densify-every 1 --no-e2e --no-cpu"
+timeout 600 $C5 > gpurun_out/plain_c5.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none -k regex:"k_densify|k_scan|k_scatter|k_block|k_gather|k_count|k_prune|k_max" -c 12 -o gpurun_out/prof_${TAG}_c5 $C5 > gpurun_out/ncu_c5.log 2>&1
 echo done

@@ -33,6 +33,16 @@ KEYS = {
     "registers": "launch__registers_per_thread",
     "sm_mhz": "smsp__cycles_elapsed.avg.per_second",
 }
+def _hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json), else the recipe's
+    fallback."""
+    try:
+        return float(json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"])
+    except Exception:
+        return 6531.9
+
+
+HBM_GBS = _hbm_peak()
 SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0,
          "us": 1e-3, "ms": 1.0, "ns": 1e-6, "s": 1e3}
 
@@ -61,6 +71,10 @@ def full(rep, out):
             k[name] = v
         if "dram_read" in k:
             k["dram_bytes_per_launch"] = k["dram_read"] + k.get("dram_write", 0)
+            if k.get("time_ms"):
+                gbs = k["dram_bytes_per_launch"] / (k["time_ms"] * 1e-3) / 1e9
+                k["dram_gbps"] = round(gbs, 1)
+                k["hbm_frac"] = round(gbs / HBM_GBS, 4)
         stalls = []
         for key, v in d.items():
             if key.startswith("smsp__pcsamp_warps_issue_stalled") and \

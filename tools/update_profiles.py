@@ -24,6 +24,13 @@ subprocess.run([sys.executable, "tools/ncu_summary.py", "launches",
                 str(prof / "ncu_launches_config2_summary.json")], check=True,
                stdout=subprocess.DEVNULL)
 shutil.copy(out / "launches.csv", prof / "ncu_launches_config2.csv")
+for suffix, name in (("_all", "ncu_full_config2_all_kernels.json"),
+                     ("_c5", "ncu_full_config5_compaction.json")):
+    rep = out / f"prof_{tag}{suffix}.ncu-rep"
+    if rep.exists():
+        subprocess.run([sys.executable, "tools/ncu_summary.py", "full",
+                        str(rep), str(prof / name)], check=True,
+                       stdout=subprocess.DEVNULL)
 full = json.loads((prof / "ncu_full_config2_fwd_adj.json").read_text())
 traffic = sum(k["dram_bytes_per_launch"] for k in full)
 Path("profiles/ncu_summary.json").write_text(json.dumps({"config2": {
