@@ -333,6 +333,76 @@ __global__ void __launch_bounds__(128) k_deform_backward(CloudView c, const doub
     }
 }
 
+// Poly+Fourier chain rule: the basis depends on t only, so one CTA tabulates
+// it per frame in shared memory; LPB lanes per ball (next power of two >= N),
+// lane n owning basis index n: no transcendental per ball and no idle lanes
+// (N = 8: 16 balls per 128-thread CTA).  Same fp64 arithmetic per lane as
+// k_deform_backward.
+template <int LPB>
+__global__ void __launch_bounds__(128) k_deform_backward_pf(CloudView c,
+                                                            const double* __restrict__ tf, int F,
+                                                            int mode, double a0_floor,
+                                                            const float* __restrict__ G,
+                                                            const float* __restrict__ Hs,
+                                                            pc_cloud_grads_t g) {
+    extern __shared__ double table[];                // (F, N)
+    const int N = c.N;
+    for (int i = threadIdx.x; i < F * N; i += blockDim.x) table[i] = pf_basis(i % N, tf[i / N]);
+    __syncthreads();
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
+    const int n = threadIdx.x % LPB;
+    if (b >= c.B) return;
+    int rows[5];
+    mode_rows(mode, rows);
+    const double a0 = c.a0[b], p0 = c.p0[b];
+    double factor[5] = {a0, p0, c.mu[3 * b], c.mu[3 * b + 1], c.mu[3 * b + 2]};
+    if (mode == PC_COORD_ADDITIVE) factor[2] = factor[3] = factor[4] = 1.0;
+    double aom[5] = {0, 0, 0, 0, 0}, gb[5] = {0, 0, 0, 0, 0};
+    for (int f = 0; f < F; ++f) {
+        const size_t s5 = 5 * ((size_t)f * c.B + b);
+        double Gs[5], H[5];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            Gs[s] = (double)G[s5 + s];
+            H[s] = (double)Hs[s5 + s];
+        }
+        const bool clamped = a0_floor > 0.0 && a0 * (1.0 + H[0]) < a0_floor;
+        double db[5];
+        if (mode == PC_COORD_ADDITIVE) {
+            db[0] = 1.0 + H[0];
+            db[1] = 1.0 + H[1];
+            db[2] = db[3] = db[4] = 1.0;
+        } else {
+#pragma unroll
+            for (int s = 0; s < 5; ++s) db[s] = 1.0 + H[rows[s]];
+        }
+        if (clamped) db[0] = 0.0;
+        double W[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            gb[s] = fma(Gs[s], db[s], gb[s]);
+            const double w = (clamped && s == 0) ? 0.0 : Gs[s] * factor[s];
+            W[rows[s]] += w;
+        }
+        if (n < N) {
+            const double ph = table[f * N + n];
+#pragma unroll
+            for (int ch = 0; ch < 5; ++ch) aom[ch] = fma(W[ch], ph, aom[ch]);
+        }
+    }
+    if (n < N) {
+#pragma unroll
+        for (int ch = 0; ch < 5; ++ch) g.omega[((size_t)b * 5 + ch) * N + n] = (float)aom[ch];
+    }
+    if (n == 0) {
+        g.a0[b] = (float)gb[0];
+        g.p0[b] = (float)gb[1];
+        g.mu[3 * b + 0] = (float)gb[2];
+        g.mu[3 * b + 1] = (float)gb[3];
+        g.mu[3 * b + 2] = (float)gb[4];
+    }
+}
+
 template <bool PC>
 static void launch_bwd(int ns, unsigned blocks, cudaStream_t st, const CloudView& c,
                        const double* tf, int F, int mode, double floor_, const float* G,
@@ -414,6 +484,16 @@ extern "C" int pc_deform_backward(const pc_cloud_t* cloud, const double* t_frame
     const unsigned blocks = (unsigned)((c.B * 32 + 127) / 128);
     cudaStream_t st = as_stream(stream);
     pc_cloud_grads_t g = *grads;
+    const size_t table_bytes = (size_t)n_frames * c.N * sizeof(double);
+    if (c.kind == PC_BASIS_POLYFOURIER && c.N <= 16 && table_bytes <= 32768) {
+        if (c.N <= 8)
+            k_deform_backward_pf<8><<<(unsigned)((c.B * 8 + 127) / 128), 128, table_bytes, st>>>(
+                c, t_frames_dev, n_frames, coord_mode, a0_floor, G, H, g);
+        else
+            k_deform_backward_pf<16><<<(unsigned)((c.B * 16 + 127) / 128), 128, table_bytes, st>>>(
+                c, t_frames_dev, n_frames, coord_mode, a0_floor, G, H, g);
+        return last_status();
+    }
     if (c.kind == PC_BASIS_GAUSS && c.per_channel)
         launch_bwd<true>(ns, blocks, st, c, t_frames_dev, n_frames, coord_mode, a0_floor, G, H, g);
     else
