@@ -30,7 +30,10 @@ namespace pc {
 // record; then the warp sweeps each surviving ball's window, lanes on
 // consecutive samples.
 
-constexpr int FWD_WARPS = 4;        // warps per forward CTA
+#ifndef PC_FWD_WARPS
+#define PC_FWD_WARPS 4
+#endif
+constexpr int FWD_WARPS = PC_FWD_WARPS;        // warps per forward CTA
 constexpr int FSW = 2;              // sensors per warp (16 lanes each)
 constexpr int FL = 32 / FSW;        // lanes per (ball, sensor) pair
 constexpr int FSTR = 2 * FL;        // samples between a lane's successive pairs
