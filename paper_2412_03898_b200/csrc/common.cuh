@@ -147,15 +147,7 @@ __device__ __forceinline__ void pair_setup(double dx, double dy, double dz, floa
              10.f * a0;
 }
 
-// Window packing for shared-memory records: jl | jh << 15 | near << 30.
-constexpr int kMaxSamples = 1 << 15;
-__device__ __forceinline__ int pack_window(int jl, int jh, bool near) {
-    return jl | (jh << 15) | (near ? (1 << 30) : 0);
-}
-__device__ __forceinline__ void unpack_window(int w, int& jl, int& jh, bool& near) {
-    jl = w & 0x7fff;
-    jh = (w >> 15) & 0x7fff;
-    near = (w >> 30) & 1;
-}
+// Longest supported trace (sample indices stay in 30 bits).
+constexpr int kMaxSamples = 1 << 30;
 
 }  // namespace pc

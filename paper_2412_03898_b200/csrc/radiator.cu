@@ -217,12 +217,6 @@ struct FwdArgs {
     int64_t chunk_balls;
 };
 
-// Record of one (ball, sensor) pair, written by its setup lane:
-//   r0 = {je0 | je1 << 15 | near << 30, X0, c, vs}  (je1 == je0: empty pair)
-//   r1 = {X at jr, Y at jr, jr, -}                 (exact / near-field only)
-// X0 = s (R - v t_je0).  The trip count is ball-uniform (from a0), so the two
-// half-warps never need to agree on it.
-
 // Both half-warps sweep the same ball for their own sensor: lane `sub` of a
 // half owns sample pairs (j, j+1), j = je0 + 2 sub + FSTR n, so each half's
 // float2 access is 128 contiguous bytes of its own trace (one conflict-free
@@ -374,7 +368,7 @@ __device__ __forceinline__ void fwd_sweep_slow(float2* __restrict__ trl, float4 
 // Per batch of 16 balls the 32 lanes set up the 16 x 2 pairs (fp32 cull,
 // fp64 geometry) into shared-memory records; then both half-warps sweep each
 // surviving ball for their own sensor (fixed ball order: deterministic).
-template <bool EXACT>
+template <bool EXACT, bool REL>
 __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -454,9 +448,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     const bool scan = s1 > s0 || (seg == 0 && dmin_box < 1e-3f);
     const float2 sub2 = make_float2((float)(2 * sub), (float)(2 * sub + 1));
     const float2 subq = make_float2((float)(2 * sub) / FSTR, (float)(2 * sub + 1) / FSTR);
-    // this half's trace at absolute sample 2 sub (s0 and je0 are even; only
-    // in-window samples are ever addressed)
-    float2* trl = reinterpret_cast<float2*>(traces + h * TP) + (sub - (s0 >> 1));
+    // this half's trace at sample 2 sub (absolute, or segment-relative with
+    // REL; s0 and je0 are even)
+    float2* trl = reinterpret_cast<float2*>(traces + h * TP) + (REL ? sub : sub - (s0 >> 1));
     FwdRec* recs = &ws.rec[h * FBATCH];
     __syncwarp();
 
@@ -494,8 +488,11 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     const int je1 = (q.jh + 1) & ~1;
                     const float X0 = fmaf((float)(q.jr - je0), vs, q.X);
                     const float D = (float)FSTR * vs;
-                    q0 = make_float4(__int_as_float(je0 | ((je1 - je0) << 15)), X0, c, -D);
-                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr), 0.f);
+                    // window start and reference sample: absolute, or relative
+                    // to the segment start for traces of 2^15 samples or more
+                    const int ib = REL ? s0 : 0;
+                    q0 = make_float4(__int_as_float((je0 - ib) | ((je1 - je0) << 15)), X0, c, -D);
+                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr - ib), 0.f);
                     const int nfull = (je1 - je0 + 1) / FSTR;
                     qr = make_float4(2.f * D, -D * D, ex2(-2.f * D * D),
                                      __int_as_float(nfull | ((je1 - je0 - nfull * FSTR) << 16)));
@@ -773,7 +770,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
 
     for (int mb = 0; mb < a.M; mb += 32) {
         const int m = mb + lane;
-        int win = 0, jr = 0;
+        int win = -1, wh = 0, jr = 0;           // window [jl, jh) (win = jl | near << 30)
         float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
         float ux = 0.f, uy = 0.f, uz = 0.f;
         if (m < a.M) {
@@ -785,7 +782,8 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             if (q.R < kCoincidenceEps) {
                 atomicMin(a.coinc, (long long)b * a.M + m);
             } else if (q.jh > q.jl) {
-                win = pack_window(q.jl, q.jh, q.near);
+                win = q.jl | (q.near ? 1 << 30 : 0);
+                wh = q.jh;
                 jr = q.jr;
                 X = q.X;
                 Y = q.Y;
@@ -802,7 +800,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
         }
         rec[lane][0] = make_float4(__int_as_float(win), __int_as_float(jr), X, kp);
         rec[lane][1] = make_float4(ka, kR1, kR2, ux);
-        rec[lane][2] = make_float4(uy, uz, Y, 0.f);
+        rec[lane][2] = make_float4(uy, uz, Y, __int_as_float(wh));
         __syncwarp();
         const int npair = min(32, a.M - mb);
         for (int pb = 0; pb < npair; pb += NGRP) {
@@ -810,10 +808,10 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             if (pi >= npair) continue;
             const float4 r0 = rec[pi][0];
             const int w = __float_as_int(r0.x);
-            if (w == 0) continue;
-            int jl, jh;
-            bool near;
-            unpack_window(w, jl, jh, near);
+            if (w < 0) continue;
+            const int jl = w & 0x3fffffff;
+            const bool near = (w >> 30) & 1;
+            const int jh = __float_as_int(rec[pi][2].w);
             // window extended to multiples of 4 (the extra samples weigh
             // < exp(-19) of the peak); lane `sub` takes quads j, j + 16, ...
             const int je1 = (jh + 3) & ~3;
@@ -992,7 +990,7 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
     ArrayConsts ac;
     if (!array_consts(array, ac) || n_balls < 0 || n_frames < 1 || !out || !coincident)
         return PC_ERR_ARGUMENT;
-    if (array->n_samples >= kMaxSamples) return PC_ERR_UNSUPPORTED;
+    if (array->n_samples >= kMaxSamples) return PC_ERR_UNSUPPORTED;   // 2^30
     const int M = array->n_sensors, T = array->n_samples, F = n_frames;
     cudaStream_t st = as_stream(stream);
     if (n_balls > 0 && (!mu_t || !a0_t || !p0_t)) return PC_ERR_ARGUMENT;
@@ -1041,15 +1039,23 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         static bool attr_set = false;
         if (!attr_set) {
             const int mx = (int)fwd_smem_bytes(fwd_tseg_max());
-            cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_forward<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_forward<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_forward<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(k_forward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             attr_set = true;
         }
         dim3 grid(p.nseg * p.nchunk, (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW), F);
-        if (ac.exact)
-            k_forward<true><<<grid, FWD_WARPS * 32, smem, st>>>(a);
+        // record windows are 15-bit: segment-relative for long traces
+        const bool rel = T >= (1 << 15) - 64;
+        if (ac.exact && rel)
+            k_forward<true, true><<<grid, FWD_WARPS * 32, smem, st>>>(a);
+        else if (ac.exact)
+            k_forward<true, false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
+        else if (rel)
+            k_forward<false, true><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         else
-            k_forward<false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
+            k_forward<false, false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         if (p.nchunk > 1) {
             k_forward_finish<<<dim3(M, F), 256, 0, st>>>(
                 partial, observed, out, want_loss ? lpart : nullptr, p.nchunk, F, M, T,
@@ -1094,7 +1100,7 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     ArrayConsts ac;
     if (!array_consts(array, ac) || n_balls < 0 || n_frames < 1 || !coincident)
         return PC_ERR_ARGUMENT;
-    if (array->n_samples >= kMaxSamples) return PC_ERR_UNSUPPORTED;
+    if (array->n_samples >= kMaxSamples) return PC_ERR_UNSUPPORTED;   // 2^30
     if (n_balls == 0) return PC_OK;
     if (!mu_t || !a0_t || !p0_t || !residual || !G) return PC_ERR_ARGUMENT;
     AdjArgs a;

@@ -78,8 +78,11 @@ def test_batched_frames_match_per_frame(pc):
         assert torch.equal(g1[0], G[f])
 
 
-def test_too_many_samples_rejected(pc):
-    arr = pc.SensorArray(np.array([[0.0, 0.0, 30.0]]), 1.5, 40.0, 32768, 0.0)
-    st = pc.CloudState(np.array([0.5]), np.array([1.0]), np.zeros((1, 3)))
-    with pytest.raises(RuntimeError):
-        pc.forward_frame(st, arr)
+def test_long_traces(pc):
+    """T beyond 2^15 samples (window indices are segment-relative in the
+    forward and full-width in the adjoint)."""
+    rng = np.random.default_rng(15)
+    pos = np.array([[0.0, 0.0, 300.0], [5.0, 0.0, 400.0], [0.0, 5.0, 600.0]])
+    arr = pc.SensorArray(pos, 1.5, 40.0, 40001, 0.0)      # 40001 samples, odd
+    a0, p0, mu = _cloud(rng, 60, 4.0, 0.2, 0.6)
+    _check_frame(pc, a0, p0, mu, arr, rng)
