@@ -1036,14 +1036,18 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         a.nchunk = p.nchunk;
         a.chunk_balls = p.chunk_balls;
         const size_t smem = fwd_smem_bytes(p.Tseg);
-        static bool attr_set = false;
-        if (!attr_set) {
+        // the dynamic shared-memory opt-in is per device: track it per device
+        static unsigned long long attr_set = 0;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return PC_ERR_CUDA;
+        const unsigned long long bit = 1ull << (dev & 63);
+        if (!(attr_set & bit)) {
             const int mx = (int)fwd_smem_bytes(fwd_tseg_max());
             cudaFuncSetAttribute(k_forward<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(k_forward<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(k_forward<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
             cudaFuncSetAttribute(k_forward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            attr_set = true;
+            attr_set |= bit;
         }
         dim3 grid(p.nseg * p.nchunk, (M + FWD_WARPS * FSW - 1) / (FWD_WARPS * FSW), F);
         // record windows are 15-bit: segment-relative for long traces
