@@ -40,12 +40,22 @@ def frame_shard(selected, rank: int, world: int) -> np.ndarray:
 def allreduce_iteration(grads, loss, coincident, group=None) -> None:
     """The iteration's exchange: SUM of the flat gradient buffer and of the
     loss, MIN of the coincidence flag (pair index, INT64_MAX = none).
-    In place; works for NCCL (device tensors) and gloo (CPU tensors)."""
+    In place; works for NCCL (device tensors) and gloo (CPU tensors).
+
+    Two collectives per iteration: the f32 gradients, and one f64 pair
+    (loss, number of ranks that saw a coincident pair); the int64 MIN runs
+    only when that count is non-zero (an error path)."""
+    import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return
     if dist.get_world_size(group) == 1:
         return
     dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(coincident, op=dist.ReduceOp.MIN, group=group)
+    int64_max = torch.iinfo(torch.int64).max
+    pair = torch.stack([loss.reshape(-1)[0].to(torch.float64),
+                        (coincident.reshape(-1)[0] != int64_max).to(torch.float64)])
+    dist.all_reduce(pair, op=dist.ReduceOp.SUM, group=group)
+    loss.reshape(-1)[0] = pair[0]
+    if float(pair[1].item()) > 0:
+        dist.all_reduce(coincident, op=dist.ReduceOp.MIN, group=group)
