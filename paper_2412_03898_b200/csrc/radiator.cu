@@ -759,7 +759,9 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     const float ka_ball = pv / (av * av * av) * inv_s * inv_s * inv_s;
     const int T = a.ac.T;
     const float D = (float)LSTRIDE * vs;
-    const bool fast = !a.ac.exact && recur_ok(D, vs, (float)a.ac.support);
+    // the MUFU sweep (mode 2) is valid for any step; the recurrence modes need
+    // their bound
+    const bool fast = !a.ac.exact && (PC_ADJ_MODE == 2 || recur_ok(D, vs, (float)a.ac.support));
     const float2 h2 = splat2(ex2(-2.f * D * D));
     const float2 mD2 = splat2(-D);
     const float2 mvs2 = splat2(-vs);
