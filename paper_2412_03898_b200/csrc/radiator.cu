@@ -686,6 +686,9 @@ constexpr int LSTRIDE = 4 * LG;   // samples between a lane's successive quads
 #ifndef PC_ADJ_CHUNK
 #define PC_ADJ_CHUNK 4
 #endif
+#ifndef PC_ADJ_LOCKSTEP
+#define PC_ADJ_LOCKSTEP 1
+#endif
 constexpr int ADJ_CHUNK = PC_ADJ_CHUNK;   // residual quads loaded per wave
 // Gaussian per chain in the sweep: 0 = both chains by recurrence, 1 = chain a
 // by MUFU and chain b by recurrence, 2 = both by MUFU.
@@ -749,8 +752,13 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * ADJ_WARPS + warp;
     const int f = blockIdx.y;
+#if PC_ADJ_LOCKSTEP
+    const bool live = b < a.B;
+    const size_t sb = (size_t)f * a.B + (live ? b : a.B - 1);
+#else
     if (b >= a.B) return;
     const size_t sb = (size_t)f * a.B + b;
+#endif
     const double mx = a.mu[3 * sb + 0], my = a.mu[3 * sb + 1], mz = a.mu[3 * sb + 2];
     const float av = a.a0[sb], pv = a.p0[sb];
     const float s = scale_of(av);
@@ -775,7 +783,11 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
         int win = -1, wh = 0, jr = 0;           // window [jl, jh) (win = jl | near << 30)
         float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
         float ux = 0.f, uy = 0.f, uz = 0.f;
+#if PC_ADJ_LOCKSTEP
+        if (live && m < a.M) {
+#else
         if (m < a.M) {
+#endif
             const double dx = mx - a.pos[3 * m + 0];
             const double dy = my - a.pos[3 * m + 1];
             const double dz = mz - a.pos[3 * m + 2];
@@ -926,7 +938,13 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             g4 = fmaf(accR, r2.y, g4);
         }
         __syncwarp();
+#if PC_ADJ_LOCKSTEP
+        __syncthreads();   // the CTA's balls read the same sensor rows together
+#endif
     }
+#if PC_ADJ_LOCKSTEP
+    if (!live) return;
+#endif
     g0 = warp_sum(g0);
     g1 = warp_sum(g1);
     g2 = warp_sum(g2);
