@@ -689,6 +689,9 @@ constexpr int LSTRIDE = 4 * LG;   // samples between a lane's successive quads
 #ifndef PC_ADJ_LOCKSTEP
 #define PC_ADJ_LOCKSTEP 1
 #endif
+#ifndef PC_ADJ_TMA
+#define PC_ADJ_TMA 0          // > 0: TMA-staged adjoint with that many balls per CTA
+#endif
 constexpr int ADJ_CHUNK = PC_ADJ_CHUNK;   // residual quads loaded per wave
 // Gaussian per chain in the sweep: 0 = both chains by recurrence, 1 = chain a
 // by MUFU and chain b by recurrence, 2 = both by MUFU.
@@ -960,6 +963,318 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- adjoint,
+// TMA-staged residual windows (PC_ADJ_TMA)
+//
+// CTA = TW balls (warps) of one frame.  Per block of 32 sensors the warps
+// set up their pairs into double-buffered records, one CTA barrier, then
+// warp 0 forms each sensor's union window over the CTA's balls and issues
+// 1-D bulk copies (cp.async.bulk, TMA) of those rows into a double-buffered
+// shared-memory stage, completing on an mbarrier; the block is then swept
+// from shared memory while the next block's copies are in flight.  The
+// mbarrier (arrive = release, wait = acquire) also publishes warp 0's union
+// offsets, so one CTA barrier per block suffices.  A block whose union does
+// not fit the stage is swept from global memory.
+
+#ifndef PC_ADJ_TSTAGE
+#define PC_ADJ_TSTAGE 8192
+#endif
+constexpr int ADJ_TSTAGE = PC_ADJ_TSTAGE;   // floats per stage buffer
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_row(float* dst, const float* src, unsigned bytes,
+                                        unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+struct StagedRow {                 // staged row: shared byte address of sample 0
+    unsigned base;
+    __device__ __forceinline__ float4 q(int j) const {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "r"(base + 4u * (unsigned)j));
+        return v;
+    }
+};
+struct GlobalRowT {
+    const float* p;
+    __device__ __forceinline__ float4 q(int j) const {
+        return __ldg(reinterpret_cast<const float4*>(p + j));
+    }
+};
+
+template <class Row>
+__device__ __forceinline__ void adj_sweep_t(const Row& row, int j, int je1, float2 xa, float2 xb,
+                                            float2 mD2, float2& A0, float2& A1, float2& A2,
+                                            float2& A3) {
+    int n = (je1 - j + LSTRIDE - 1) / LSTRIDE;
+#define PC_T_STEP(R)                                     \
+    accum_pair_mufu(lo2(R), xa, A0, A1, A2, A3);         \
+    accum_pair_mufu(hi2(R), xb, A0, A1, A2, A3);         \
+    xa = fadd2(xa, mD2);                                 \
+    xb = fadd2(xb, mD2);
+    for (; n >= 4; n -= 4, j += 4 * LSTRIDE) {
+        float4 rr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rr[u] = row.q(j + u * LSTRIDE);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            PC_T_STEP(rr[u])
+        }
+    }
+    if (n > 0) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 q0 = row.q(j);
+        const float4 q1 = n > 1 ? row.q(j + LSTRIDE) : z;
+        const float4 q2 = n > 2 ? row.q(j + 2 * LSTRIDE) : z;
+        PC_T_STEP(q0)
+        if (n > 1) {
+            PC_T_STEP(q1)
+        }
+        if (n > 2) {
+            PC_T_STEP(q2)
+        }
+    }
+#undef PC_T_STEP
+}
+
+template <class Row>
+__device__ __forceinline__ void adj_sweep_direct_t(const Row& row, int j, int je1, float2 k,
+                                                   float vs, float X, float Y, bool near,
+                                                   float2& A0, float2& A1, float2& A2,
+                                                   float2& A3) {
+    const float2 two = splat2(2.f), kstep = splat2((float)LSTRIDE);
+    const float2 mvs2 = splat2(-vs), vs2 = splat2(vs);
+    for (; j < je1; j += LSTRIDE) {
+        const float4 r = row.q(j);
+        const float2 kb = fadd2(k, two);
+        const float2 xa = ffma2(k, mvs2, splat2(X));
+        const float2 xb = ffma2(kb, mvs2, splat2(X));
+        accum_pair(lo2(r), ex2n_2(fmul2(xa, xa)), xa, A0, A1, A2, A3);
+        accum_pair(hi2(r), ex2n_2(fmul2(xb, xb)), xb, A0, A1, A2, A3);
+        if (near) {
+            const float2 ya = ffma2(k, vs2, splat2(Y));
+            const float2 yb = ffma2(kb, vs2, splat2(Y));
+            accum_pair(lo2(r), ex2n_2(fmul2(ya, ya)), ya, A0, A1, A2, A3);
+            accum_pair(hi2(r), ex2n_2(fmul2(yb, yb)), yb, A0, A1, A2, A3);
+        }
+        k = fadd2(k, kstep);
+    }
+}
+
+template <int TW>
+__global__ void __launch_bounds__(TW * 32) k_adjoint_tma(AdjArgs a) {
+    extern __shared__ __align__(128) unsigned char tsm[];
+    float* stage = reinterpret_cast<float*>(tsm);                        // [2][ADJ_TSTAGE]
+    float4(*recs)[TW][32][3] =
+        reinterpret_cast<float4(*)[TW][32][3]>(stage + 2 * ADJ_TSTAGE);  // [2][TW][32][3]
+    int2(*s_win)[32] = reinterpret_cast<int2(*)[32]>(recs + 2);          // [TW][32]
+    int* s_lo = reinterpret_cast<int*>(s_win + TW);                       // [2][32]
+    int* s_off = s_lo + 64;                                               // [2][33]
+    unsigned long long* bar =
+        reinterpret_cast<unsigned long long*>(((uintptr_t)(s_off + 66) + 7) & ~(uintptr_t)7);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * TW + warp;
+    const bool live = b < a.B;
+    const int f = blockIdx.y;
+    const size_t sb = (size_t)f * a.B + (live ? b : a.B - 1);
+    const double mx = a.mu[3 * sb + 0], my = a.mu[3 * sb + 1], mz = a.mu[3 * sb + 2];
+    const float av = a.a0[sb], pv = a.p0[sb];
+    const float s = scale_of(av);
+    const float vs = a.ac.vdt * s;
+    const float inv_s = 1.f / s;
+    const float ka_ball = pv / (av * av * av) * inv_s * inv_s * inv_s;
+    const int T = a.ac.T;
+    const float2 mD2 = splat2(-(float)LSTRIDE * vs);
+    const float2 mvs2 = splat2(-vs);
+    float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f;
+    const int grp = lane / LG, sub = lane % LG;
+    const int nblk = (a.M + 31) / 32;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto setup = [&](int kb, int buf) {
+        const int m = kb * 32 + lane;
+        int win = -1, wh = 0, jr = 0;
+        float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
+        float ux = 0.f, uy = 0.f, uz = 0.f;
+        int2 wq = make_int2(0x7fffffff, -0x7fffffff);
+        if (live && m < a.M) {
+            const double dx = mx - a.pos[3 * m + 0];
+            const double dy = my - a.pos[3 * m + 1];
+            const double dz = mz - a.pos[3 * m + 2];
+            PairSetup q;
+            pair_setup(dx, dy, dz, av, s, a.ac, 0, T, q);
+            if (q.R < kCoincidenceEps) {
+                atomicMin(a.coinc, (long long)b * a.M + m);
+            } else if (q.jh > q.jl) {
+                win = q.jl | (q.near ? 1 << 30 : 0);
+                wh = q.jh;
+                wq = make_int2(q.jl & ~3, (q.jh + 3) & ~3);
+                jr = q.jr;
+                X = q.X;
+                Y = q.Y;
+                const double ir = 1.0 / q.R;
+                const float inv2R = (float)(0.5 * ir);
+                kp = inv2R * inv_s;
+                ka = ka_ball * inv2R;
+                kR2 = pv * inv2R;
+                kR1 = -kR2 * (float)ir * inv_s;
+                ux = (float)(dx * ir);
+                uy = (float)(dy * ir);
+                uz = (float)(dz * ir);
+            }
+        }
+        recs[buf][warp][lane][0] = make_float4(__int_as_float(win), __int_as_float(jr), X, kp);
+        recs[buf][warp][lane][1] = make_float4(ka, kR1, kR2, ux);
+        recs[buf][warp][lane][2] = make_float4(uy, uz, Y, __int_as_float(wh));
+        s_win[warp][lane] = wq;
+    };
+    // warp 0: union windows of block kb, offsets, bulk copies (or none)
+    auto issue = [&](int kb, int buf) {
+        int lo = 0x7fffffff, hi = -0x7fffffff;
+#pragma unroll
+        for (int w2 = 0; w2 < TW; ++w2) {
+            lo = min(lo, s_win[w2][lane].x);
+            hi = max(hi, s_win[w2][lane].y);
+        }
+        const int len = hi > lo ? hi - lo : 0;
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const bool fits = total <= ADJ_TSTAGE;
+        s_lo[buf * 32 + lane] = len ? lo : 0;
+        s_off[buf * 33 + lane] = incl - len;
+        if (lane == 0) s_off[buf * 33 + 32] = fits ? total : -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive_tx(&bar[buf], fits ? (unsigned)total * 4u : 0u);
+        __syncwarp();
+        if (fits && len > 0) {
+            const int m = kb * 32 + lane;
+            tma_row(stage + buf * ADJ_TSTAGE + (incl - len),
+                    a.resid + ((size_t)f * a.M + m) * T + lo, (unsigned)len * 4u, &bar[buf]);
+        }
+    };
+
+    setup(0, 0);
+    __syncthreads();
+    if (warp == 0) issue(0, 0);
+    unsigned phase[2] = {0u, 0u};
+    for (int kb = 0; kb < nblk; ++kb) {
+        const int buf = kb & 1;
+        if (kb + 1 < nblk) {
+            setup(kb + 1, buf ^ 1);
+            __syncthreads();       // all warps are past block kb-1: its buffers are free
+            if (warp == 0) issue(kb + 1, buf ^ 1);
+        }
+        mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const bool staged = s_off[buf * 33 + 32] >= 0;
+        const int mb = kb * 32;
+        const int npair = min(32, a.M - mb);
+        if (live) {
+            for (int pb = 0; pb < npair; pb += NGRP) {
+                const int pi = pb + grp;
+                if (pi >= npair) continue;
+                const float4 r0 = recs[buf][warp][pi][0];
+                const int w = __float_as_int(r0.x);
+                if (w < 0) continue;
+                const int jl = w & 0x3fffffff;
+                const bool near = (w >> 30) & 1;
+                const float4 r2 = recs[buf][warp][pi][2];
+                const int jh = __float_as_int(r2.w);
+                const int je1 = (jh + 3) & ~3;
+                const int j = (jl & ~3) + 4 * sub;
+                float2 A0 = splat2(0.f), A1 = A0, A2 = A0, A3 = A0;
+                if (j < je1) {
+                    const int jrr = __float_as_int(r0.y);
+                    const float2 k = make_float2((float)(j - jrr), (float)(j + 1 - jrr));
+                    const float2 xa = ffma2(k, mvs2, splat2(r0.z));
+                    const float2 xb = ffma2(fadd2(k, splat2(2.f)), mvs2, splat2(r0.z));
+                    if (staged) {
+                        const StagedRow row{smem_u32(stage + buf * ADJ_TSTAGE) +
+                                            4u * (unsigned)(s_off[buf * 33 + pi] -
+                                                            s_lo[buf * 32 + pi])};
+                        if (!near)
+                            adj_sweep_t(row, j, je1, xa, xb, mD2, A0, A1, A2, A3);
+                        else
+                            adj_sweep_direct_t(row, j, je1, k, vs, r0.z, r2.z, true, A0, A1, A2,
+                                               A3);
+                    } else {
+                        const GlobalRowT row{a.resid + ((size_t)f * a.M + mb + pi) * T};
+                        if (!near)
+                            adj_sweep_t(row, j, je1, xa, xb, mD2, A0, A1, A2, A3);
+                        else
+                            adj_sweep_direct_t(row, j, je1, k, vs, r0.z, r2.z, true, A0, A1, A2,
+                                               A3);
+                    }
+                }
+                const float a1 = A1.x + A1.y, a3 = A3.x + A3.y;
+                const float aq = fmaf(A2.x + A2.y, -kKappa, A0.x + A0.y);
+                const float4 r1 = recs[buf][warp][pi][1];
+                const float accR = fmaf(r1.y, a1, r1.z * aq);
+                g0 = fmaf(r1.x, a3, g0);
+                g1 = fmaf(r0.w, a1, g1);
+                g2 = fmaf(accR, r1.w, g2);
+                g3 = fmaf(accR, r2.x, g3);
+                g4 = fmaf(accR, r2.y, g4);
+            }
+        }
+        __syncwarp();
+    }
+    if (!live) return;
+    g0 = warp_sum(g0);
+    g1 = warp_sum(g1);
+    g2 = warp_sum(g2);
+    g3 = warp_sum(g3);
+    g4 = warp_sum(g4);
+    if (lane == 0) {
+        float* out = a.G + 5 * sb;
+        out[0] = g0;
+        out[1] = g1;
+        out[2] = g2;
+        out[3] = g3;
+        out[4] = g4;
+    }
+}
+
+template <int TW>
+static size_t adj_tma_smem() {
+    return 2 * ADJ_TSTAGE * sizeof(float) + 2 * TW * 32 * 3 * sizeof(float4) +
+           TW * 32 * sizeof(int2) + (64 + 66) * sizeof(int) + 16 + 16;
+}
+
 static bool array_consts(const pc_array_t* arr, ArrayConsts& ac) {
     if (!arr || !arr->positions || arr->n_sensors < 1 || arr->n_samples < 1 ||
         !(arr->sound_speed > 0) || !(arr->dt > 0))
@@ -1141,6 +1456,24 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     a.ac = ac;
     dim3 grid((unsigned)((n_balls + ADJ_WARPS - 1) / ADJ_WARPS), n_frames);
     cudaStream_t st = as_stream(stream);
+#if PC_ADJ_TMA
+    if (!ac.exact && array->n_samples % 4 == 0 &&
+        reinterpret_cast<uintptr_t>(residual) % 16 == 0) {
+        constexpr int TW = PC_ADJ_TMA;
+        const size_t smem = adj_tma_smem<TW>();
+        static unsigned long long tma_attr = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(tma_attr & (1ull << (dev & 63)))) {
+            cudaFuncSetAttribute(k_adjoint_tma<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            tma_attr |= 1ull << (dev & 63);
+        }
+        dim3 gt((unsigned)((n_balls + TW - 1) / TW), n_frames);
+        k_adjoint_tma<TW><<<gt, TW * 32, smem, st>>>(a);
+        return last_status();
+    }
+#endif
     if (array->n_samples % 4 == 0 && reinterpret_cast<uintptr_t>(residual) % 16 == 0)
         k_adjoint<true><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
     else
