@@ -40,6 +40,10 @@ constexpr int FSTR = 2 * FL;        // samples between a lane's successive pairs
 constexpr int FBATCH = 32 / FSW;    // balls per setup batch (one lane per pair)
 constexpr int FWD_TSEG_MAX = 1024;  // samples per time segment (private traces)
 constexpr int64_t FWD_CHUNK_BALLS = 16384;            // balls per forward chunk (max)
+#ifndef PC_FWD_MIN_CHUNK
+#define PC_FWD_MIN_CHUNK 128
+#endif
+constexpr int64_t FWD_MIN_CHUNK_BALLS = PC_FWD_MIN_CHUNK; // balls per forward chunk (min)
 constexpr size_t FWD_PARTIAL_BUDGET = (size_t)16 << 30;  // bytes of chunk partial traces
 constexpr int TRACE_PAD = 8;        // floats after a trace (even-window overrun)
 
@@ -97,7 +101,7 @@ static FwdPlan fwd_plan(int64_t B, int F, int M, int T) {
     if (c < c_box) c = c_box;
     const char* ce = getenv("PC_FWD_CHUNKS");      // tuning override
     if (ce && atoi(ce) > 0) c = atoi(ce);
-    const int64_t cmax = B / 256 > 1 ? B / 256 : 1;
+    const int64_t cmax = B / FWD_MIN_CHUNK_BALLS > 1 ? B / FWD_MIN_CHUNK_BALLS : 1;
     if (c > cmax) c = cmax;
     if (c > 64) c = 64;
     const size_t per_chunk = (size_t)F * M * T * sizeof(float);
@@ -963,6 +967,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     }
 }
 
+#if PC_ADJ_TMA
 // ---------------------------------------------------------------- adjoint,
 // TMA-staged residual windows (PC_ADJ_TMA)
 //
@@ -1274,6 +1279,8 @@ static size_t adj_tma_smem() {
     return 2 * ADJ_TSTAGE * sizeof(float) + 2 * TW * 32 * 3 * sizeof(float4) +
            TW * 32 * sizeof(int2) + (64 + 66) * sizeof(int) + 16 + 16;
 }
+
+#endif  // PC_ADJ_TMA
 
 static bool array_consts(const pc_array_t* arr, ArrayConsts& ac) {
     if (!arr || !arr->positions || arr->n_sensors < 1 || arr->n_samples < 1 ||
