@@ -230,6 +230,23 @@ int pc_adam_segments(double *params, const float *grads, double *m,
                      const double *seg_lr, const int32_t *seg_step,
                      const double *seg_floor, pc_stream_t stream);
 
+/* The iteration's update without a host round trip: Adam (optimizer 0) or
+ * SGD (1) over n_seg segments like pc_adam_segments / pc_sgd_segments, with
+ * each segment's (lr, step t) read from hyper_dev (device, 2*n_seg doubles)
+ * and the reference's guard semantics decided on the device: nothing is
+ * updated if *coincident_dev != INT64_MAX or *loss_dev is not finite
+ * (radiator.py:186-192, reconstruction.py:317-318); otherwise the segments
+ * whose group (seg_group, host, in update order) precedes the first group
+ * with a non-finite flag (flags_dev, from pc_check_finite) are updated
+ * (reconstruction.py:60-61, 320-327).  seg_off / seg_floor / seg_group are
+ * host arrays. */
+int pc_update_guarded(double *params, const float *grads, double *m,
+                      double *v, int32_t n_seg, const int64_t *seg_off,
+                      const double *seg_floor, const int32_t *seg_group,
+                      const double *hyper_dev, const int32_t *flags_dev,
+                      const double *loss_dev, const int64_t *coincident_dev,
+                      int32_t optimizer, pc_stream_t stream);
+
 /* Replaces reconstruction.py:72-76 sgd_step over segments. */
 int pc_sgd_segments(double *params, const float *grads, int32_t n_seg,
                     const int64_t *seg_off, const double *seg_lr,

@@ -80,6 +80,9 @@ SIGNATURES = {
     "pc_backproject": (c_int32, [_P, _P, c_int32, c_int32, c_double, c_double,
                                  c_double, POINTER(c_double), c_double,
                                  POINTER(c_int32), _P, _P]),
+    "pc_update_guarded": (c_int32, [_P, _P, _P, _P, c_int32, POINTER(c_int64),
+                                    POINTER(c_double), POINTER(c_int32), _P,
+                                    _P, _P, _P, c_int32, _P]),
     "pc_l2_loss": (c_int32, [_P, _P, c_int64, _P, _P]),
     "pc_check_finite": (c_int32, [_P, c_int32, POINTER(c_int64), _P, _P]),
     "pc_adam_segments": (c_int32, [_P, _P, _P, _P, c_int32, POINTER(c_int64),

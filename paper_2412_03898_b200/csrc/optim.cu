@@ -369,6 +369,81 @@ extern "C" int pc_adam_segments(double* params, const float* grads, double* m, d
     return last_status();
 }
 
+// Guarded update (no host round trip between the gradient and the step):
+// every block reads the non-finite flags, the iteration loss and the
+// coincidence word from the device and applies the reference's semantics --
+// a coincident pair or a non-finite loss raise before any update
+// (radiator.py:186-192, reconstruction.py:317-318), a non-finite gradient
+// raises after the groups before it were stepped (reconstruction.py:60-61,
+// 320-327) -- so the host only reads the status once the step is done.
+struct GuardTable {
+    int64_t off[PC_MAX_SEGMENTS + 1];
+    double floor_[PC_MAX_SEGMENTS];
+    int group[PC_MAX_SEGMENTS];
+    int n;
+};
+
+__global__ void __launch_bounds__(256) k_update_guarded(double* __restrict__ p,
+                                                        const float* __restrict__ g,
+                                                        double* __restrict__ m,
+                                                        double* __restrict__ v, GuardTable t,
+                                                        const double* __restrict__ hyper,
+                                                        const int* __restrict__ flags,
+                                                        const double* __restrict__ loss,
+                                                        const long long* __restrict__ coinc,
+                                                        int sgd) {
+    const int s = blockIdx.y;
+    int bad = 0x7fffffff;
+    for (int k = 0; k < t.n; ++k)
+        if (flags[k]) bad = min(bad, t.group[k]);
+    if (!isfinite(*loss) || *coinc != 0x7fffffffffffffffLL || t.group[s] >= bad) return;
+    const int64_t lo = t.off[s], hi = t.off[s + 1];
+    const double lr = hyper[2 * s], step = hyper[2 * s + 1], fl = t.floor_[s];
+    const double bc1 = 1.0 - pow(kBeta1, step), bc2 = 1.0 - pow(kBeta2, step);
+    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double gi = (double)g[i];
+        double pi;
+        if (sgd) {
+            pi = p[i] - lr * gi;
+        } else {
+            double mi = m[i] * kBeta1;
+            mi = mi + (1.0 - kBeta1) * gi;
+            double vi = v[i] * kBeta2;
+            vi = vi + (1.0 - kBeta2) * gi * gi;
+            m[i] = mi;
+            v[i] = vi;
+            pi = p[i] - lr * (mi / bc1) / (sqrt(vi / bc2) + kEps);
+        }
+        p[i] = pi < fl ? fl : pi;
+    }
+}
+
+extern "C" int pc_update_guarded(double* params, const float* grads, double* m, double* v,
+                                 int32_t n_seg, const int64_t* seg_off, const double* seg_floor,
+                                 const int32_t* seg_group, const double* hyper_dev,
+                                 const int32_t* flags_dev, const double* loss_dev,
+                                 const int64_t* coincident_dev, int32_t optimizer,
+                                 pc_stream_t stream) {
+    SegTable st;
+    if (!seg_table(n_seg, seg_off, st) || !seg_group || !hyper_dev || !flags_dev || !loss_dev ||
+        !coincident_dev || (optimizer != 0 && optimizer != 1))
+        return PC_ERR_ARGUMENT;
+    if (st.off[n_seg] > st.off[0] && (!params || !grads || (optimizer == 0 && (!m || !v))))
+        return PC_ERR_ARGUMENT;
+    GuardTable t;
+    t.n = n_seg;
+    for (int k = 0; k <= n_seg; ++k) t.off[k] = seg_off[k];
+    for (int k = 0; k < n_seg; ++k) {
+        t.floor_[k] = seg_floor ? seg_floor[k] : -INFINITY;
+        t.group[k] = seg_group[k];
+    }
+    k_update_guarded<<<dim3(seg_blocks(st), n_seg), 256, 0, as_stream(stream)>>>(
+        params, grads, m, v, t, hyper_dev, flags_dev, loss_dev,
+        reinterpret_cast<const long long*>(coincident_dev), optimizer);
+    return last_status();
+}
+
 extern "C" int pc_sgd_segments(double* params, const float* grads, int32_t n_seg,
                                const int64_t* seg_off, const double* seg_lr,
                                const double* seg_floor, pc_stream_t stream) {

@@ -196,6 +196,8 @@ class IterationEngine:
                                       device=self.device)
         self.host_observed = None
         self._copy_stream = None
+        self._hyper_host = None
+        self._hyper_dev = None
         # frame groups for forward / adjoint overlap (PC_FRAME_GROUPS)
         self.frame_groups = int(os.environ.get("PC_FRAME_GROUPS", "1"))
         self._adj_stream = None
@@ -439,21 +441,73 @@ class IterationEngine:
                 _lib.f64_array([floors.get(s.name, -math.inf)]),
                 _lib.stream()), "pc_sgd_segments")
 
-    def iterate(self, iteration: int, frames: np.ndarray) -> float:
-        """One full iteration; returns the (all-reduced) loss."""
+    def _lrs(self, iteration: int) -> dict:
         cfg = self.cfg
-        lrs = {"coords": scheduled_lr(cfg.lr_coords, iteration,
-                                      cfg.step_size, cfg.drop_rate),
-               "pressure": scheduled_lr(cfg.lr_pressure, iteration,
-                                        cfg.step_size, cfg.drop_rate),
-               "std": scheduled_lr(cfg.lr_std, iteration, cfg.step_size,
-                                   cfg.drop_rate),
-               "deform": scheduled_lr(cfg.lr_deform, iteration,
-                                      cfg.step_size, cfg.drop_rate)}
+        return {"coords": scheduled_lr(cfg.lr_coords, iteration,
+                                       cfg.step_size, cfg.drop_rate),
+                "pressure": scheduled_lr(cfg.lr_pressure, iteration,
+                                         cfg.step_size, cfg.drop_rate),
+                "std": scheduled_lr(cfg.lr_std, iteration, cfg.step_size,
+                                    cfg.drop_rate),
+                "deform": scheduled_lr(cfg.lr_deform, iteration,
+                                       cfg.step_size, cfg.drop_rate)}
+
+    def _guarded_update(self, lrs: dict) -> None:
+        """pc_check_finite + pc_update_guarded: the step and its guard on
+        the device, (lr, t) per segment from a pinned table copied with the
+        launch; the host learns the outcome from the one status read."""
+        lib = _lib.load_library()
+        segs = self.layout.segments
+        n = len(segs)
+        if self._hyper_host is None or self._hyper_host.numel() != 2 * n:
+            self._hyper_host = torch.empty(2 * n, dtype=torch.float64).pin_memory()
+            self._hyper_dev = torch.empty(2 * n, dtype=torch.float64,
+                                          device=self.device)
+        hv = self._hyper_host.numpy()
+        for i, sg in enumerate(segs):
+            hv[2 * i] = lrs[sg.group]
+            hv[2 * i + 1] = self.step_count[sg.name] + 1
+        self._hyper_dev.copy_(self._hyper_host, non_blocking=True)
+        cfg = self.cfg
+        floors = {"p0": cfg.p0_floor, "a0": cfg.a0_floor,
+                  "sigma": cfg.sigma_floor}
+        off = _lib.i64_array(self.layout.offsets)
+        self.flags.zero_()
+        _lib.check(lib.pc_check_finite(
+            _lib.ptr(self.Gf), n, off, _lib.ptr(self.flags), _lib.stream()),
+            "pc_check_finite")
+        _lib.check(lib.pc_update_guarded(
+            _lib.ptr(self.P), _lib.ptr(self.Gf), _lib.ptr(self.Mo),
+            _lib.ptr(self.Vo), n, off,
+            _lib.f64_array([floors.get(sg.name, -math.inf) for sg in segs]),
+            _lib.i32_array([GROUP_ORDER.index(sg.group) for sg in segs]),
+            _lib.ptr(self._hyper_dev), _lib.ptr(self.flags),
+            _lib.ptr(self.loss_total), _lib.ptr(self.coinc),
+            0 if cfg.optimizer == "adam" else 1, _lib.stream()),
+            "pc_update_guarded")
+
+    def _status(self):
+        status = torch.cat([self.loss_total, self.flags.double(),
+                            self.coinc.double()]).cpu().numpy()
+        loss = float(status[0])
+        flags = status[1:1 + len(self.layout.segments)].astype(bool)
+        # pair indices b*M+m stay far below 2**53; INT64_MAX means "none"
+        coinc = int(status[-1]) if status[-1] < 9.0e18 else _lib.INT64_MAX
+        return loss, flags, coinc
+
+    def iterate(self, iteration: int, frames: np.ndarray) -> float:
+        """One full iteration; returns the (all-reduced) loss.
+
+        gradient -> (all-reduce) -> finite guard -> guarded Adam all stay on
+        the device; the host reads the status once, after the step, and
+        raises the reference's exceptions (the device applied exactly the
+        updates the reference makes before raising)."""
+        lrs = self._lrs(iteration)
         self.last_lrs = lrs
         self.compute_grads(frames)
         self.allreduce()
-        loss, flags, coinc = self.check_and_status()
+        self._guarded_update(lrs)
+        loss, flags, coinc = self._status()
         if coinc != _lib.INT64_MAX:
             b, m = divmod(coinc, self.darr.M)
             raise_if_coincident(int(self.order[b]) * self.darr.M + m,
@@ -461,20 +515,16 @@ class IterationEngine:
                                 self.darr.positions)
         if not math.isfinite(loss):
             raise RuntimeError(f"non-finite loss at iteration {iteration}")
+        bad = len(GROUP_ORDER)
         if flags.any():
-            # reference order: groups before the first bad one are updated
-            bad_groups = {self.layout.segments[i].group
-                          for i in np.nonzero(flags)[0]}
-            done = []
-            for g in GROUP_ORDER:
-                names = [s.name for s in self.layout.segments
-                         if s.group == g]
-                if g in bad_groups:
-                    self.apply_update(lrs, only=done)
-                    raise ValueError(
-                        f"non-finite gradient in parameter group '{g}'")
-                done += names
-        self.apply_update(lrs)
+            bad = min(GROUP_ORDER.index(self.layout.segments[i].group)
+                      for i in np.nonzero(flags)[0])
+        for sg in self.layout.segments:        # the segments stepped
+            if GROUP_ORDER.index(sg.group) < bad:
+                self.step_count[sg.name] += 1
+        if bad < len(GROUP_ORDER):
+            raise ValueError(
+                f"non-finite gradient in parameter group '{GROUP_ORDER[bad]}'")
         return loss
 
     # ------------------------------------------------------------ densify

@@ -537,3 +537,76 @@ def test_growth_loop_runs_and_grows(pc):
             eng.densify(p0_min=0.01, q=90.0, max_balls=1200)
             sizes.append(eng.B)
     assert sizes[-1] > sizes[0] and sizes[-1] <= 1200
+
+
+# ------------------------------------------------------------ engine guards
+
+def _guard_engine(pc):
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.engine import IterationEngine
+    prob = synth.make_problem(2, n_balls=300, n_sensors=32, n_frames=3)
+    obs = _observed(prob)
+    return prob, IterationEngine(prob.cloud, prob.array, obs,
+                                 prob.frame_times, prob.config)
+
+
+def _segs(eng):
+    return {s.name: eng.P[s.offset:s.offset + s.size].clone()
+            for s in eng.layout.segments}
+
+
+def test_engine_nonfinite_gradient_updates_earlier_groups_only(pc):
+    """reconstruction.py:60-61, 320-327: the groups before the first bad one
+    are stepped, then ValueError names the bad group (decided on the device,
+    no host round trip before the step)."""
+    prob, eng = _guard_engine(pc)
+    eng.iterate(0, np.arange(prob.n_frames))          # a clean step first
+    before, steps = _segs(eng), dict(eng.step_count)
+    mu = eng.layout.by_name["mu"]
+    orig = eng.allreduce
+
+    def poison():
+        orig()
+        eng.Gf[mu.offset + 7] = float("nan")
+    eng.allreduce = poison
+    with pytest.raises(ValueError, match="coords"):
+        eng.iterate(1, np.arange(prob.n_frames))
+    after = _segs(eng)
+    for name in ("p0", "a0"):
+        assert not np.array_equal(after[name].cpu(), before[name].cpu()), name
+        assert eng.step_count[name] == steps[name] + 1
+    for name in ("mu", "omega"):
+        assert np.array_equal(after[name].cpu(), before[name].cpu()), name
+        assert eng.step_count[name] == steps[name]
+
+
+def test_engine_nonfinite_loss_updates_nothing(pc):
+    prob, eng = _guard_engine(pc)
+    before, steps = _segs(eng), dict(eng.step_count)
+    orig = eng.allreduce
+
+    def poison():
+        orig()
+        eng.loss_total.fill_(float("inf"))
+    eng.allreduce = poison
+    with pytest.raises(RuntimeError, match="non-finite loss"):
+        eng.iterate(0, np.arange(prob.n_frames))
+    after = _segs(eng)
+    assert all(np.array_equal(after[k].cpu(), before[k].cpu()) for k in after)
+    assert eng.step_count == steps
+
+
+def test_engine_coincidence_updates_nothing(pc):
+    from paper_2412_03898_b200.engine import IterationEngine
+    from paper_2412_03898_b200 import synth
+    prob = synth.make_problem(2, n_balls=200, n_sensors=16, n_frames=2)
+    cloud = prob.cloud
+    cloud.mu[5] = prob.array.positions[3]             # ball 5 on sensor 3
+    cloud.omega[5] = 0.0                              # and not deformed away
+    eng = IterationEngine(cloud, prob.array, _observed(prob),
+                          prob.frame_times, prob.config, spatial_order=False)
+    before = _segs(eng)
+    with pytest.raises(ValueError, match=r"ball 5 coincides with sensor 3"):
+        eng.iterate(0, np.arange(prob.n_frames))
+    after = _segs(eng)
+    assert all(np.array_equal(after[k].cpu(), before[k].cpu()) for k in after)
