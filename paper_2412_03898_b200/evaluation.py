@@ -153,10 +153,11 @@ def normalize_pair(a, b):
 
 def gaussian_window(size: int = SSIM_WINDOW,
                     sigma: float = SSIM_SIGMA) -> np.ndarray:
-    r = np.arange(size, dtype=np.float64) - (size - 1) / 2.0
-    g = np.exp(-0.5 * (r / sigma) ** 2)
-    w = np.outer(g, g)
-    return w / w.sum()
+    """Unit-sum separable Gaussian window (size x size)."""
+    half = (size - 1) / 2.0
+    g1 = np.exp(-0.5 * ((np.arange(size) - half) / sigma) ** 2)
+    g1 /= g1.sum()
+    return np.outer(g1, g1)
 
 
 def _window_mean(img: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
@@ -175,51 +176,43 @@ def ssim(a, b, data_range: float = 1.0) -> float:
         raise ValueError(
             f"images must be at least {SSIM_WINDOW} pixels per side")
     dev = _device() if torch.cuda.is_available() else torch.device("cpu")
-    ta = torch.as_tensor(av, device=dev)
-    tb = torch.as_tensor(bv, device=dev)
-    w = torch.as_tensor(gaussian_window(), device=dev)
-    c1 = (SSIM_K1 * data_range) ** 2
-    c2 = (SSIM_K2 * data_range) ** 2
-    mu_a, mu_b = _window_mean(ta, w), _window_mean(tb, w)
-    var_a = _window_mean(ta * ta, w) - mu_a * mu_a
-    var_b = _window_mean(tb * tb, w) - mu_b * mu_b
-    cov = _window_mean(ta * tb, w) - mu_a * mu_b
-    num = (2.0 * mu_a * mu_b + c1) * (2.0 * cov + c2)
-    den = (mu_a * mu_a + mu_b * mu_b + c1) * (var_a + var_b + c2)
-    return float((num / den).mean().item())
+    x, y = torch.as_tensor(av, device=dev), torch.as_tensor(bv, device=dev)
+    win = torch.as_tensor(gaussian_window(), device=dev)
+    stab1, stab2 = (SSIM_K1 * data_range) ** 2, (SSIM_K2 * data_range) ** 2
+    # local moments: E[x], E[y], E[x^2], E[y^2], E[xy] over each window
+    ex, ey, exx, eyy, exy = (_window_mean(t, win)
+                             for t in (x, y, x * x, y * y, x * y))
+    luminance = (2.0 * ex * ey + stab1) / (ex * ex + ey * ey + stab1)
+    structure = (2.0 * (exy - ex * ey) + stab2) / \
+        ((exx - ex * ex) + (eyy - ey * ey) + stab2)
+    return float((luminance * structure).mean().item())
 
 
 def eval_report(recon_grids, truth_grids, ubp_grids=None) -> list:
     """Per-frame, per-axis SSIM of MAP images against ground truth, methods
     "4d" (and "ubp"), each pair normalised by its joint maximum."""
-    recon_grids, truth_grids = list(recon_grids), list(truth_grids)
-    if len(recon_grids) != len(truth_grids):
-        raise ValueError("frame counts of recon and truth differ")
-    methods = {"4d": recon_grids}
+    truth = list(truth_grids)
+    runs = [("4d", list(recon_grids))]
     if ubp_grids is not None:
-        ubp_grids = list(ubp_grids)
-        if len(ubp_grids) != len(truth_grids):
-            raise ValueError("frame counts of ubp and truth differ")
-        methods["ubp"] = ubp_grids
-    out = []
-    for k, truth in enumerate(truth_grids):
-        for axis in MAP_AXES:
-            t_map = map_project(truth, axis)
-            for name, grids in methods.items():
-                rn, tn = normalize_pair(map_project(grids[k], axis), t_map)
-                out.append({"frame": k, "axis": axis, "method": name,
-                            "ssim": ssim(rn, tn)})
-    return out
+        runs.append(("ubp", list(ubp_grids)))
+    for name, grids in runs:
+        if len(grids) != len(truth):
+            what = "recon" if name == "4d" else name
+            raise ValueError(f"frame counts of {what} and truth differ")
+    return [{"frame": k, "axis": ax, "method": name,
+             "ssim": ssim(*normalize_pair(map_project(grids[k], ax),
+                                          map_project(truth[k], ax)))}
+            for k in range(len(truth)) for ax in MAP_AXES
+            for name, grids in runs]
 
 
 def format_report(records) -> str:
     """Aligned text table of an eval_report result."""
-    methods = sorted({r["method"] for r in records})
-    frames = sorted({r["frame"] for r in records})
-    val = {(r["frame"], r["axis"], r["method"]): r["ssim"] for r in records}
-    cols = [f"{m}/{ax}" for m in methods for ax in MAP_AXES]
-    lines = ["frame  " + "  ".join(f"{c:>10s}" for c in cols)]
-    for k in frames:
-        lines.append(f"{k:5d}  " + "  ".join(
-            f"{val[(k, ax, m)]:10.4f}" for m in methods for ax in MAP_AXES))
-    return "\n".join(lines)
+    table = {(r["frame"], r["axis"], r["method"]): r["ssim"] for r in records}
+    methods = sorted({m for _, _, m in table})
+    header = [f"{m}/{ax}" for m in methods for ax in MAP_AXES]
+    out = ["frame  " + "  ".join(h.rjust(10) for h in header)]
+    for k in sorted({f for f, _, _ in table}):
+        row = [table[(k, ax, m)] for m in methods for ax in MAP_AXES]
+        out.append(f"{k:5d}  " + "  ".join(f"{v:10.4f}" for v in row))
+    return "\n".join(out)
