@@ -34,7 +34,10 @@ namespace pc {
 #define PC_FWD_WARPS 4
 #endif
 constexpr int FWD_WARPS = PC_FWD_WARPS;        // warps per forward CTA
-constexpr int FSW = 2;              // sensors per warp (16 lanes each)
+#ifndef PC_FWD_FSW
+#define PC_FWD_FSW 2
+#endif
+constexpr int FSW = PC_FWD_FSW;     // sensors per warp (32 / FSW lanes each)
 constexpr int FL = 32 / FSW;        // lanes per (ball, sensor) pair
 constexpr int FSTR = 2 * FL;        // samples between a lane's successive pairs
 constexpr int FBATCH = 32 / FSW;    // balls per setup batch (one lane per pair)
@@ -419,8 +422,11 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             dmin = 3.4e38f;
             dmax = 0.f;
         }
-        dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, FL));
-        dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, FL));
+#pragma unroll
+        for (int o = FL; o < 32; o <<= 1) {
+            dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+            dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        }
         dmin_box = dmin;
         const float w = sup * amax;
         const double tlo = (((double)dmin - w) * a.ac.inv_v - a.ac.t0) * a.ac.inv_dt;
@@ -509,8 +515,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 // {X, Y, jr}), else the recurrence when its bounds hold
                 // (bit 31, record 1 = {2D, -D^2, h, nfull | tail << 16})
                 // (the shuffle must run on every lane: no short-circuit)
-                const bool pslow = __shfl_xor_sync(0xffffffffu, slow, FL);
-                const bool bslow = slow || pslow;
+                bool bslow = slow;
+#pragma unroll
+                for (int o = FL; o < 32; o <<= 1)
+                    bslow = __shfl_xor_sync(0xffffffffu, bslow, o) || bslow;
                 int w = __float_as_int(q0.x);
                 if (bslow) {
                     w |= 1 << 30;
@@ -526,7 +534,10 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             // compact: balls with a live pair for either sensor, in batch order
             const unsigned pm = __ballot_sync(0xffffffffu, pass);
             const bool anyslow = __any_sync(0xffffffffu, slow);
-            const unsigned bm = (pm | (pm >> FL)) & ((1u << FL) - 1u);
+            unsigned bm = pm;
+#pragma unroll
+            for (int o = FL; o < 32; o <<= 1) bm |= bm >> o;
+            bm &= (1u << FL) - 1u;
             if ((bm >> sub) & 1u) {
                 const int pos = __popc(bm & ((1u << sub) - 1u));
                 recs[pos].r0 = q0;

@@ -1,0 +1,14 @@
+# Build a variant of libpacloud_b200.so with extra nvcc defines into
+# build/variants/NAME.so (select it with PACLOUD_B200_LIB=...).
+# usage: tools/build_variant.sh NAME "-DPC_X=1 -DPC_Y=2"
+set -e
+NAME=$1; DEFS=$2
+ROOT=$(cd "$(dirname "$0")/.." && pwd)
+C=$ROOT/paper_2412_03898_b200/csrc
+OUT=$ROOT/build/variants/$NAME
+mkdir -p $OUT
+ARCH="-gencode arch=compute_100a,code=sm_100a"
+FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include $DEFS"
+nvcc $FL -Xptxas -v -c $C/radiator.cu -o $OUT/radiator.o 2>&1 | grep -A2 "k_forwardILb0ELb0E\|k_adjointILb1" | grep -E "registers|spill" || true
+nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/$NAME.so $OUT/radiator.o $C/deform.o $C/optim.o $C/voxel.o $C/ubp.o
+echo built build/variants/$NAME.so
