@@ -688,7 +688,7 @@ constexpr int LG = PC_ADJ_LG;             // lanes per pair (adjoint; 1 / 2 / 4 
 constexpr int NGRP = 32 / LG;     // pairs in flight per warp
 constexpr int LSTRIDE = 4 * LG;   // samples between a lane's successive quads
 #ifndef PC_ADJ_CHUNK
-#define PC_ADJ_CHUNK 4
+#define PC_ADJ_CHUNK 2        // config 2 adjoint ms: 1 / 2 / 3 / 4 -> 5.49 / 4.90 / 4.98 / 5.11
 #endif
 #ifndef PC_ADJ_LOCKSTEP
 #define PC_ADJ_LOCKSTEP 1
