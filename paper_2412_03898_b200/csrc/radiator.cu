@@ -753,6 +753,9 @@ __device__ __forceinline__ void accum_pair_mufu(float2 r, float2 x, float2& A0, 
     A3 = ffma2(u, x, A3);
 }
 
+// Registers: ptxas's default for 128-thread blocks gives 64 (8 CTAs / SM);
+// config 2 adjoint ms at 96 / 64 / 56 / 48 registers (min-blocks 1 / none /
+// 9 / 10): 5.43 / 4.90 / 5.66 / 5.62.
 template <bool ALIGNED>
 __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     __shared__ __align__(16) float4 recs[ADJ_WARPS][32][3];
