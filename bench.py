@@ -437,8 +437,9 @@ def run_ours(args, rank, world, local):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": e2e_pairs / args.steps / (ems * 1e-3), "unit": UNIT,
-               "ms_per_step": ems, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": 8 + 4 * len(eng.layout.segments) + 8,
+               "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d) + eng._hyper_host.numel() * eng._hyper_host.element_size(),
+               "d2h_bytes_per_step": eng._status_host.numel() * eng._status_host.element_size(),
                "api": "IterationEngine.iterate with the step's observed frames "
                       "uploaded from pinned host memory (stream_observed_from)"}
         eng.stream_observed_from(None)

@@ -187,6 +187,11 @@ class IterationEngine:
         self._warmed = False
         self._graph = None
         self._graph_frames = None
+        self._tail_graph = None
+        self._tail_key = None
+        self._tail_warmed = False
+        self._status_host = None
+        self._status_dev = None
         self._bufs_F = -1
         n_seg = len(self.layout.segments)
         self.flags = torch.zeros(n_seg, dtype=torch.int32, device=self.device)
@@ -452,21 +457,31 @@ class IterationEngine:
                 "deform": scheduled_lr(cfg.lr_deform, iteration,
                                        cfg.step_size, cfg.drop_rate)}
 
-    def _guarded_update(self, lrs: dict) -> None:
-        """pc_check_finite + pc_update_guarded: the step and its guard on
-        the device, (lr, t) per segment from a pinned table copied with the
-        launch; the host learns the outcome from the one status read."""
-        lib = _lib.load_library()
+    def _fill_hyper(self, lrs: dict) -> None:
+        """(lr, t) per segment into the pinned table the update copies."""
         segs = self.layout.segments
         n = len(segs)
         if self._hyper_host is None or self._hyper_host.numel() != 2 * n:
             self._hyper_host = torch.empty(2 * n, dtype=torch.float64).pin_memory()
             self._hyper_dev = torch.empty(2 * n, dtype=torch.float64,
                                           device=self.device)
+            self._status_host = torch.empty(n + 2, dtype=torch.float64).pin_memory()
+            self._status_dev = torch.empty(n + 2, dtype=torch.float64,
+                                           device=self.device)
+            self._tail_graph = None
         hv = self._hyper_host.numpy()
         for i, sg in enumerate(segs):
             hv[2 * i] = lrs[sg.group]
             hv[2 * i + 1] = self.step_count[sg.name] + 1
+
+    def _launch_tail(self) -> None:
+        """pc_check_finite + pc_update_guarded: the step and its guard on
+        the device, (lr, t) per segment from the pinned table (copied in
+        stream order), then the status (loss, flags, coincidence) packed and
+        copied to pinned host memory; no host synchronisation here."""
+        lib = _lib.load_library()
+        segs = self.layout.segments
+        n = len(segs)
         self._hyper_dev.copy_(self._hyper_host, non_blocking=True)
         cfg = self.cfg
         floors = {"p0": cfg.p0_floor, "a0": cfg.a0_floor,
@@ -485,12 +500,43 @@ class IterationEngine:
             _lib.ptr(self.loss_total), _lib.ptr(self.coinc),
             0 if cfg.optimizer == "adam" else 1, _lib.stream()),
             "pc_update_guarded")
+        self._status_dev[0:1].copy_(self.loss_total)
+        self._status_dev[1:1 + n].copy_(self.flags)
+        self._status_dev[n + 1:n + 2].copy_(self.coinc)
+        self._status_host.copy_(self._status_dev, non_blocking=True)
+
+    def _guarded_update(self, lrs: dict) -> None:
+        """Guard + update + status copy, replayed from a CUDA graph once the
+        layout is fixed (one launch instead of seven eager ones)."""
+        self._fill_hyper(lrs)
+        key = (self.P.data_ptr(), self.Gf.data_ptr(), self.Mo.data_ptr(),
+               self.Vo.data_ptr(), self.layout.total,
+               self._status_host.data_ptr())
+        if not self.use_graph:
+            self._launch_tail()
+            return
+        if self._tail_graph is not None and self._tail_key == key:
+            self._tail_graph.replay()
+            return
+        if not self._tail_warmed:
+            self._launch_tail()          # eager once (lazy library init)
+            self._tail_warmed = True
+            return
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream(device=self.device)
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                self._launch_tail()
+        torch.cuda.current_stream().wait_stream(st)
+        self._tail_graph, self._tail_key = g, key
+        g.replay()
 
     def _status(self):
-        status = torch.cat([self.loss_total, self.flags.double(),
-                            self.coinc.double()]).cpu().numpy()
+        torch.cuda.current_stream().synchronize()
+        status = self._status_host.numpy()
         loss = float(status[0])
-        flags = status[1:1 + len(self.layout.segments)].astype(bool)
+        flags = status[1:-1].astype(bool)
         # pair indices b*M+m stay far below 2**53; INT64_MAX means "none"
         coinc = int(status[-1]) if status[-1] < 9.0e18 else _lib.INT64_MAX
         return loss, flags, coinc
