@@ -399,6 +399,16 @@ def run_ours(args, rank, world, local):
         "mufu_frac": 2.0 * S / ((t_fwd + t_adj) * 1e-3) /
         (148 * 16 * 1965e6),
         "peak_source": peak_src,
+        # the algorithm's pipe ceiling: forward bound by
+        # the shared-memory float2 read-modify-write and adjoint by the
+        # FMA/MUFU balance, both measured at ~16 in-support samples / clk /
+        # SM (tools/ubench/pipes.cu, profiles/r1/ubench_pipes_b200.txt)
+        "pipe_ceiling": {
+            "frac": FLOPS_PER_SAMPLE * 8.0 / 256.0,
+            "frac_achieved_of_ceiling": (achieved / peak) / (FLOPS_PER_SAMPLE * 8.0 / 256.0),
+            "samples_per_clk_per_sm": S / ((t_fwd + t_adj) * 1e-3) / (148 * 1965e6),
+            "ceiling_samples_per_clk_per_sm": 8.0,
+        },
     }
 
     # ---- e2e: the user-facing call with host buffers (pinned observed in,

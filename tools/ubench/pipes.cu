@@ -73,6 +73,59 @@ __global__ void kbench(float* out, float s) {
     if (acc == 1234.5f) out[threadIdx.x] = acc;
 }
 
+// Shared-memory read-modify-write of float2 (the forward's trace update):
+// each warp owns a 2 KB trace, lane l updates samples 2l, 2l+1 of 64-sample
+// steps (one conflict-free 256-byte LDS.64 + STS.64 per warp step).
+__global__ void ksmem(float* out, float s) {
+    __shared__ float2 tr[8][256];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int i = l; i < 256; i += 32) tr[w][i] = make_float2(0.f, 0.f);
+    __syncwarp();
+    const float2 c = make_float2(s, s * 0.5f);
+    for (int it = 0; it < NIT; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float2* p = &tr[w][(k * 32 + l + it) & 255];   // address varies per iteration
+            float2 t;
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(t.x), "=f"(t.y)
+                         : "r"((unsigned)__cvta_generic_to_shared(p)));
+            t.x += c.x;
+            t.y += c.y;
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" :: "r"((unsigned)__cvta_generic_to_shared(p)),
+                         "f"(t.x), "f"(t.y) : "memory");
+        }
+    }
+    __syncwarp();
+    float acc = 0.f;
+    for (int i = l; i < 256; i += 32) acc += tr[w][i].x + tr[w][i].y;
+    if (acc == 1234.5f) out[threadIdx.x] = acc;
+}
+
+void run_smem() {
+    float* out;
+    cudaMalloc(&out, 4096);
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = nsm * 8, threads = 256;
+    ksmem<<<blocks, threads>>>(out, 1.f);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; ++r) ksmem<<<blocks, threads>>>(out, 1.f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    // samples updated: 2 per lane per RMW
+    const double samples = 5.0 * blocks * threads * (double)NIT * 8 * 2;
+    const double cycles = ms * 1e-3 * clk * 1e3;
+    printf("%-28s %.3f samples/clk/SM  (%.3f ms)\n", "smem float2 RMW", samples / cycles / nsm, ms);
+    cudaFree(out);
+}
+
 template <int K>
 void run(const char* name, int ops_per_inner) {
     float* out;
@@ -108,5 +161,6 @@ int main() {
     run<6>("FADD", 1);
     run<7>("FFMA2+MUFU (pairs)", 2);
     run<8>("FMUL2+FADD (pairs)", 2);
+    run_smem();
     return 0;
 }
