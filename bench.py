@@ -338,6 +338,8 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    if os.environ.get("PC_BENCH_DEBUG"):
+        print("step ms", [round(x, 3) for x in step_ms], "B", eng.B, file=sys.stderr)
     ms = float(np.mean(step_ms))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -441,7 +443,11 @@ def run_ours(args, rank, world, local):
             ee[k][1].record()
             it += 1
         torch.cuda.synchronize()
-        ems = float(np.mean([a.elapsed_time(b) for a, b in ee]))
+        e2e_step_ms = [a.elapsed_time(b) for a, b in ee]
+        if os.environ.get("PC_BENCH_DEBUG"):
+            print("e2e step ms", [round(x, 3) for x in e2e_step_ms], "B", eng.B,
+                  file=sys.stderr)
+        ems = float(np.mean(e2e_step_ms))
         if world > 1:
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
