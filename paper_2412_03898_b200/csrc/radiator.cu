@@ -231,11 +231,15 @@ struct FwdArgs {
 // Gaussian term of one sample pair: x 2^(-x^2)
 __device__ __forceinline__ float2 gterm(float2 x) { return fmul2(x, ex2n_2(fmul2(x, x))); }
 
-// Record word 0: je0 | span << 15 | slow << 30 | recur << 31 (span = je1 - je0,
-// even; per ball: slow = a pair of the ball needs the near field (or exact),
-// recur = the Gaussian may be stepped by recurrence, recur_ok).
-__device__ __forceinline__ int rec_je0(int w) { return w & 0x7fff; }
-__device__ __forceinline__ int rec_span(int w) { return (w >> 15) & 0x7fff; }
+// Record word 0: byte offset of sample je0 in the warp's trace area (this
+// half's trace, segment-relative; even je0) | slow << 30 | recur << 31 (per
+// ball: slow = a pair of the ball needs the near field (or exact), recur =
+// the Gaussian may be stepped by recurrence, recur_ok).  The lane adds its own
+// 8 sub once, so a sweep's pointer is one add (p = lane_base + offset).
+constexpr int REC_OFF_MASK = (1 << 20) - 1;
+__device__ __forceinline__ float2* rec_ptr(unsigned char* lbase, int w) {
+    return reinterpret_cast<float2*>(lbase + (w & REC_OFF_MASK));
+}
 
 // Fast path.  r0 = {word, X0, c, dx} with X0 = x at je0 and dx = -FSTR s v dt.
 // Lane `sub` covers samples je0 + 2 sub + FSTR k; the first (span + 1) / FSTR
@@ -243,14 +247,14 @@ __device__ __forceinline__ int rec_span(int w) { return (w >> 15) & 0x7fff; }
 // live on the lower lanes.  trl = this half's trace at absolute sample 2 sub;
 // subq = 2 sub / FSTR (exact: x0 = X0 + subq dx = X0 - 2 sub s v dt).  In a
 // block of 4 steps x_k = x_b + k dx, x_b += 4 dx.
-__device__ __forceinline__ void fwd_sweep_fast(float2* __restrict__ trl, float4 r0, int sub2i,
-                                               float2 subq) {
+__device__ __forceinline__ void fwd_sweep_fast(unsigned char* lbase, float4 r0, float4 r1,
+                                               int sub2i, float2 subq) {
     const int w = __float_as_int(r0.x);
-    const int span = rec_span(w);
+    const int span = __float_as_int(r1.w);
     const float2 dx = splat2(r0.w);
     const float2 cc = splat2(r0.z);
     float2 xb = ffma2(subq, dx, splat2(r0.y));
-    float2* p = trl + (rec_je0(w) >> 1);
+    float2* __restrict__ p = rec_ptr(lbase, w);
     const int nfull = (span + 1) / FSTR;
     int n = nfull;
     const float2 k2 = fadd2(dx, dx), k3 = fadd2(k2, dx), k4 = fadd2(k2, k2);
@@ -291,7 +295,7 @@ __device__ __forceinline__ void fwd_sweep_fast(float2* __restrict__ trl, float4 
 // fwd_sweep_fast (r0.w = dx = -D); r1 = {2D, -D^2, h, nfull | tail << 16}
 // from the setup pass: nfull steps are live on every lane of the half, one
 // more where 2 sub < tail.
-__device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4 r0, float4 r1,
+__device__ __forceinline__ void fwd_sweep_recur(unsigned char* lbase, float4 r0, float4 r1,
                                                 int sub2i, float2 subq) {
     const int w = __float_as_int(r0.x);
     const int nr = __float_as_int(r1.w);
@@ -301,7 +305,7 @@ __device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4
     float2 e = ex2n_2(fmul2(x, x));
     float2 g = ex2_2(ffma2(x, splat2(r1.x), splat2(r1.y)));
     const float2 h2 = splat2(r1.z);
-    float2* p = trl + (rec_je0(w) >> 1);
+    float2* __restrict__ p = rec_ptr(lbase, w);
     const int nfull = nr & 0xffff;
     int n = nfull;
 #define PC_FWD_RSTEP(V)   \
@@ -333,17 +337,15 @@ __device__ __forceinline__ void fwd_sweep_recur(float2* __restrict__ trl, float4
 // Exact window / near field: x (and y) from the exact integer offset to the
 // wavefront sample jr every iteration (the window may start far from it).
 // r1 = {X, Y at jr, jr, h}; s v dt = -r0.w / FSTR (exact).
-__device__ __forceinline__ void fwd_sweep_slow(float2* __restrict__ trl, float4 r0, float4 r1,
+__device__ __forceinline__ void fwd_sweep_slow(unsigned char* lbase, float4 r0, float4 r1,
                                                float2 sub2, int sub2i) {
     const int w = __float_as_int(r0.x);
-    const int je0 = rec_je0(w);
     const bool near = (w >> 30) & 1;        // the ball's slow flag: evaluate the near field
-    const int nl = (rec_span(w) - sub2i + FSTR - 1) / FSTR;
+    const int nl = (__float_as_int(r1.w) - sub2i + FSTR - 1) / FSTR;
     const float vs = r0.w * (-1.f / FSTR);
     const float2 cc = splat2(r0.z);
-    const int jr = __float_as_int(r1.z);
-    float2 k = fadd2(sub2, splat2((float)(je0 - jr)));
-    float2* p = trl + (je0 >> 1);
+    float2 k = fadd2(sub2, splat2((float)__float_as_int(r1.z)));   // je0 - jr
+    float2* p = rec_ptr(lbase, w);
     for (int n = 0; n < nl; ++n, p += FL) {
         const float2 x = ffma2(k, splat2(-vs), splat2(r1.x));
         float2 v = fmul2(x, ex2n_2(fmul2(x, x)));
@@ -454,9 +456,9 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
         sq_tab[warp][lane] = make_float2((float)(2 * lane) / FSTR, (float)(2 * lane + 1) / FSTR);
     __syncwarp();
     const float2 subq = sq_tab[warp][sub];
-    // this half's trace at sample 2 sub (absolute, or segment-relative with
-    // REL; s0 and je0 are even)
-    float2* trl = reinterpret_cast<float2*>(traces + h * TP) + (REL ? sub : sub - (s0 >> 1));
+    // the warp's trace area at this lane's first sample pair (records carry
+    // this half's segment-relative byte offsets)
+    unsigned char* lbase = reinterpret_cast<unsigned char*>(traces) + 8 * sub;
     FwdRec* recs = &ws.rec[h * FBATCH];
     __syncwarp();
 
@@ -494,11 +496,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                     const int je1 = (q.jh + 1) & ~1;
                     const float X0 = fmaf((float)(q.jr - je0), vs, q.X);
                     const float D = (float)FSTR * vs;
-                    // window start and reference sample: absolute, or relative
-                    // to the segment start for traces of 2^15 samples or more
-                    const int ib = REL ? s0 : 0;
-                    q0 = make_float4(__int_as_float((je0 - ib) | ((je1 - je0) << 15)), X0, c, -D);
-                    q1 = make_float4(q.X, q.Y, __int_as_float(q.jr - ib), 0.f);
+                    // trace byte offset of je0 (this half, segment-relative);
+                    // record 1 for the direct forms: {X, Y, je0 - jr, span}
+                    const int off = (je0 - s0) * 4 + h * TP * 4;
+                    q0 = make_float4(__int_as_float(off), X0, c, -D);
+                    q1 = make_float4(q.X, q.Y, __int_as_float(je0 - q.jr),
+                                     __int_as_float(je1 - je0));
                     const int nfull = (je1 - je0 + 1) / FSTR;
                     qr = make_float4(2.f * D, -D * D, ex2(-2.f * D * D),
                                      __int_as_float(nfull | ((je1 - je0 - nfull * FSTR) << 16)));
@@ -545,11 +548,11 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 const float4 r0 = recs[k].r0;
                 const int w = __float_as_int(r0.x);
                 if (w < 0)
-                    fwd_sweep_recur(trl, r0, recs[k].r1, 2 * sub, subq);
+                    fwd_sweep_recur(lbase, r0, recs[k].r1, 2 * sub, subq);
                 else if (EXACT || (anyslow && ((w >> 30) & 1)))
-                    fwd_sweep_slow(trl, r0, recs[k].r1, sub2, 2 * sub);
+                    fwd_sweep_slow(lbase, r0, recs[k].r1, sub2, 2 * sub);
                 else
-                    fwd_sweep_fast(trl, r0, 2 * sub, subq);
+                    fwd_sweep_fast(lbase, r0, recs[k].r1, 2 * sub, subq);
                 __syncwarp();
             }
         }
