@@ -798,7 +798,8 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     float4(&rec)[32][3] = recs[warp];
     const int grp = lane / LG, sub = lane % LG;
 
-    for (int mb = 0; mb < a.M; mb += 32) {
+    const float* rblk = a.resid + (size_t)f * a.M * T;     // this block's first row
+    for (int mb = 0; mb < a.M; mb += 32, rblk += (size_t)32 * T) {
         const int m = mb + lane;
         int win = -1, wh = 0, jr = 0;           // window [jl, jh) (win = jl | near << 30)
         float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             // < exp(-19) of the peak); lane `sub` takes quads j, j + 16, ...
             const int je1 = (jh + 3) & ~3;
             int j = (jl & ~3) + 4 * sub;
-            const float* row = a.resid + ((size_t)f * a.M + mb + pi) * T;
+            const float* row = rblk + (size_t)pi * T;
             float2 A0 = splat2(0.f), A1 = A0, A2 = A0, A3 = A0;
             if (j < je1) {
                 const int jrr = __float_as_int(r0.y);
