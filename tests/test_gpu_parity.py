@@ -539,6 +539,33 @@ def test_growth_loop_runs_and_grows(pc):
     assert sizes[-1] > sizes[0] and sizes[-1] <= 1200
 
 
+def test_graphs_through_densify_bit_identical_to_eager(pc):
+    """The compute graph and the guard/update/status graph are re-captured
+    after every layout change (densify swaps the parameter buffers); the
+    replayed iterations must equal eager launches bit for bit."""
+    import torch
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.engine import IterationEngine
+    prob = synth.make_problem(5, seed=11, n_balls=700, n_sensors=40,
+                              n_frames=4)
+    obs = np.stack([oracle.forward_frame(oracle.States(a, p, m), prob.array)
+                    for a, p, m in prob.gt_frames]).astype(np.float32)
+    engs = [IterationEngine(prob.cloud, prob.array, obs, prob.frame_times,
+                            prob.config, spatial_order=False, use_graph=g)
+            for g in (True, False)]
+    frames = np.arange(prob.n_frames)
+    for it in range(7):
+        losses = [e.iterate(it, frames) for e in engs]
+        assert losses[0] == losses[1]
+        if it % 3 == 2:
+            for e in engs:
+                e.densify(p0_min=0.01, q=90.0, max_balls=1100)
+    assert engs[0].B == engs[1].B > 700
+    assert torch.equal(engs[0].P, engs[1].P)
+    assert torch.equal(engs[0].Mo, engs[1].Mo)
+    assert torch.equal(engs[0].Vo, engs[1].Vo)
+
+
 # ------------------------------------------------------------ engine guards
 
 def _guard_engine(pc):
