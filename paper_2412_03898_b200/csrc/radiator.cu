@@ -724,6 +724,7 @@ struct AdjArgs {
     int64_t B;
     int F, M;
     ArrayConsts ac;
+    int msplit;     // SPLIT: first sensor of the second half (multiple of 32)
 };
 
 // Residual samples j .. j+3 (one 16-byte load when rows are 16-byte aligned).
@@ -766,12 +767,20 @@ __device__ __forceinline__ void accum_pair_mufu(float2 r, float2 x, float2& A0, 
 // Registers: ptxas's default for 128-thread blocks gives 64 (8 CTAs / SM);
 // config 2 adjoint ms at 96 / 64 / 56 / 48 registers (min-blocks 1 / none /
 // 9 / 10): 5.43 / 4.90 / 5.66 / 5.62.
-template <bool ALIGNED>
+//
+// SPLIT (small problems, < 2 waves of CTAs): each ball's sensors are split
+// over two CTAs (blockIdx.y = 2 frame + half, halves on 32-sensor blocks),
+// which add their partial G into the zeroed output; with exactly two
+// addends onto 0 the sum is order-independent (IEEE addition commutes), so
+// the result stays deterministic.
+template <bool ALIGNED, bool SPLIT>
 __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     __shared__ __align__(16) float4 recs[ADJ_WARPS][32][3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * ADJ_WARPS + warp;
-    const int f = blockIdx.y;
+    const int f = SPLIT ? (int)(blockIdx.y >> 1) : (int)blockIdx.y;
+    const int m_lo = SPLIT ? (int)(blockIdx.y & 1) * a.msplit : 0;
+    const int m_hi = SPLIT ? ((blockIdx.y & 1) ? a.M : min(a.M, a.msplit)) : a.M;
 #if PC_ADJ_LOCKSTEP
     const bool live = b < a.B;
     const size_t sb = (size_t)f * a.B + (live ? b : a.B - 1);
@@ -798,14 +807,14 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     float4(&rec)[32][3] = recs[warp];
     const int grp = lane / LG, sub = lane % LG;
 
-    const float* rblk = a.resid + (size_t)f * a.M * T;     // this block's first row
-    for (int mb = 0; mb < a.M; mb += 32, rblk += (size_t)32 * T) {
+    const float* rblk = a.resid + ((size_t)f * a.M + m_lo) * T;   // this block's first row
+    for (int mb = m_lo; mb < m_hi; mb += 32, rblk += (size_t)32 * T) {
         const int m = mb + lane;
         int win = -1, wh = 0, jr = 0;           // window [jl, jh) (win = jl | near << 30)
         float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
         float ux = 0.f, uy = 0.f, uz = 0.f;
 #if PC_ADJ_LOCKSTEP
-        if (live && m < a.M) {
+        if (live && m < m_hi) {
 #else
         if (m < a.M) {
 #endif
@@ -837,7 +846,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
         rec[lane][1] = make_float4(ka, kR1, kR2, ux);
         rec[lane][2] = make_float4(uy, uz, Y, __int_as_float(wh));
         __syncwarp();
-        const int npair = min(32, a.M - mb);
+        const int npair = min(32, m_hi - mb);
         for (int pb = 0; pb < npair; pb += NGRP) {
             const int pi = pb + grp;
             if (pi >= npair) continue;
@@ -973,11 +982,19 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     g4 = warp_sum(g4);
     if (lane == 0) {
         float* out = a.G + 5 * sb;
-        out[0] = g0;
-        out[1] = g1;
-        out[2] = g2;
-        out[3] = g3;
-        out[4] = g4;
+        if (SPLIT) {
+            atomicAdd(out + 0, g0);
+            atomicAdd(out + 1, g1);
+            atomicAdd(out + 2, g2);
+            atomicAdd(out + 3, g3);
+            atomicAdd(out + 4, g4);
+        } else {
+            out[0] = g0;
+            out[1] = g1;
+            out[2] = g2;
+            out[3] = g3;
+            out[4] = g4;
+        }
     }
 }
 
@@ -1453,6 +1470,16 @@ extern "C" int pc_residual_loss(const float* predicted, const float* observed, f
     return last_status();
 }
 
+// Two-CTA sensor split of the adjoint for small grids (PC_ADJ_SPLIT=0 off).
+static bool adj_split() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PC_ADJ_SPLIT");
+        v = e ? atoi(e) != 0 : 1;
+    }
+    return v != 0;
+}
+
 extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, const float* p0_t,
                                        int64_t n_balls, int32_t n_frames,
                                        const pc_array_t* array, const float* residual, float* G,
@@ -1495,9 +1522,24 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
         return last_status();
     }
 #endif
-    if (array->n_samples % 4 == 0 && reinterpret_cast<uintptr_t>(residual) % 16 == 0)
-        k_adjoint<true><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
-    else
-        k_adjoint<false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+    // fewer than two waves of 8-CTA SMs: split each ball's sensors over two
+    // CTAs (G zeroed, two partial sums added)
+    const int64_t ctas = ((n_balls + ADJ_WARPS - 1) / ADJ_WARPS) * n_frames;
+    const bool split = adj_split() && a.M >= 64 && ctas < 2LL * 8 * num_sms();
+    a.msplit = ((a.M / 2 + 31) / 32) * 32;
+    const bool aligned = array->n_samples % 4 == 0 && reinterpret_cast<uintptr_t>(residual) % 16 == 0;
+    if (split) {
+        if (cudaMemsetAsync(G, 0, (size_t)n_balls * n_frames * 5 * sizeof(float), st) != cudaSuccess)
+            return PC_ERR_CUDA;
+        dim3 g2(grid.x, 2 * n_frames);
+        if (aligned)
+            k_adjoint<true, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
+        else
+            k_adjoint<false, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
+    } else if (aligned) {
+        k_adjoint<true, false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+    } else {
+        k_adjoint<false, false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+    }
     return last_status();
 }
