@@ -599,6 +599,93 @@ static int finish_vec(const void* a, const void* b, const void* c, int T) {
 // and every base pointer 16-byte aligned, checked on the host), scalar
 // otherwise.  HBM-bound: (nchunk + 2) x 4 B/sample.
 // (out may alias partial when nchunk == 1: element-wise, same thread)
+// Chunk combine that reads each chunk's partial row only over the samples
+// sensor m can receive from that chunk: the arrival range of the (frame,
+// chunk) bounding box seen from sensor m, as k_forward computes it for its
+// warp (which covers it), widened by 4 samples.  Outside that range the
+// forward wrote exact zeros, so skipping them leaves every per-sample sum in
+// the same chunk order and bit-identical to k_forward_finish, while the
+// traffic scales with the arrival ranges instead of nchunk x T (64 chunks at
+// one frame per rank).  Thread t owns samples j = t (mod 256) of a
+// shared-memory tile; no barriers between chunks.
+constexpr int CMB_TILE = 4096;
+__global__ void __launch_bounds__(256) k_forward_combine(const float* __restrict__ partial,
+                                                         const unsigned* __restrict__ bounds,
+                                                         const double* __restrict__ pos,
+                                                         ArrayConsts ac,
+                                                         const float* __restrict__ obs,
+                                                         float* __restrict__ out,
+                                                         double* __restrict__ loss, int nchunk,
+                                                         int F, int M, int T) {
+    __shared__ float acc[CMB_TILE];
+    __shared__ int2 rg[64];
+    const int m = blockIdx.x, f = blockIdx.y;
+    const int tid = threadIdx.x;
+    const size_t row = ((size_t)f * M + m) * T;
+    const size_t cstride = (size_t)F * M * T;
+    if (tid < nchunk) {
+        const float fpx = (float)pos[3 * m], fpy = (float)pos[3 * m + 1], fpz = (float)pos[3 * m + 2];
+        const unsigned* bf = bounds + 8 * ((size_t)f * nchunk + tid);
+        const float lx = ord2f(bf[0]), ly = ord2f(bf[1]), lz = ord2f(bf[2]);
+        const float hx = ord2f(~bf[3]), hy = ord2f(~bf[4]), hz = ord2f(~bf[5]);
+        const float amax = ord2f(~bf[6]);
+        const float nx = fmaxf(fmaxf(lx - fpx, fpx - hx), 0.f);
+        const float ny = fmaxf(fmaxf(ly - fpy, fpy - hy), 0.f);
+        const float nz = fmaxf(fmaxf(lz - fpz, fpz - hz), 0.f);
+        const float fx = fmaxf(fabsf(lx - fpx), fabsf(hx - fpx));
+        const float fy = fmaxf(fabsf(ly - fpy), fabsf(hy - fpy));
+        const float fz = fmaxf(fabsf(lz - fpz), fabsf(hz - fpz));
+        const float dmin = sqrtf(nx * nx + ny * ny + nz * nz);
+        const float dmax = sqrtf(fx * fx + fy * fy + fz * fz);
+        const float w = (float)ac.support * amax;
+        const double tlo = (((double)dmin - w) * ac.inv_v - ac.t0) * ac.inv_dt;
+        const double thi = (((double)dmax + w) * ac.inv_v - ac.t0) * ac.inv_dt;
+        const double pad = 6.0 + 1e-5 * (double)dmax * ac.inv_v * ac.inv_dt;
+        int lo = (int)fmax(0.0, fmin((double)T, floor(tlo - pad)));
+        int hi = (int)fmax((double)lo, fmin((double)T, ceil(thi + pad)));
+        if (bf[0] == ~0u) lo = hi = 0;          // empty chunk (no balls)
+        rg[tid] = make_int2(lo, hi);
+    }
+    __syncthreads();
+    double lsum = 0.0;
+    for (int t0 = 0; t0 < T; t0 += CMB_TILE) {
+        const int t1 = min(T, t0 + CMB_TILE);
+        for (int j = t0 + tid; j < t1; j += 256) acc[j - t0] = 0.f;
+        for (int c = 0; c < nchunk; ++c) {
+            const int lo = max(rg[c].x, t0), hi = min(rg[c].y, t1);
+            const float* pc = partial + c * cstride + row;
+            int j = lo + ((t0 + tid - lo) & 255);      // first owned sample >= lo
+            for (; j + 3 * 256 < hi; j += 4 * 256) {
+                const float v0 = __ldcs(pc + j), v1 = __ldcs(pc + j + 256);
+                const float v2 = __ldcs(pc + j + 512), v3 = __ldcs(pc + j + 768);
+                acc[j - t0] += v0;
+                acc[j - t0 + 256] += v1;
+                acc[j - t0 + 512] += v2;
+                acc[j - t0 + 768] += v3;
+            }
+            for (; j < hi; j += 256) acc[j - t0] += __ldcs(pc + j);
+        }
+        for (int j = t0 + tid; j < t1; j += 256) {
+            float s = acc[j - t0];
+            if (obs) {
+                s -= __ldcs(obs + row + j);
+                lsum = fma((double)s, (double)s, lsum);
+            }
+            out[row + j] = s;
+        }
+    }
+    if (!loss) return;
+    __shared__ double red[8];
+    lsum = warp_sum(lsum);
+    if ((tid & 31) == 0) red[tid >> 5] = lsum;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int wq = 0; wq < 8; ++wq) t += red[wq];
+        loss[(size_t)f * M + m] = t;
+    }
+}
+
 __global__ void __launch_bounds__(256, 4) k_forward_finish(const float* partial,
                                                            const float* __restrict__ obs,
                                                            float* out, double* __restrict__ loss,
@@ -1333,6 +1420,16 @@ static bool array_consts(const pc_array_t* arr, ArrayConsts& ac) {
 
 using namespace pc;
 
+// Range-limited chunk combine (PC_FWD_CMB=0 selects the dense combine).
+static bool fwd_cmb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PC_FWD_CMB");
+        v = e ? atoi(e) != 0 : 1;
+    }
+    return v != 0;
+}
+
 extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array_t* array,
                                int32_t* plan) {
     if (!array || !plan || n_balls < 0 || n_frames < 1 || array->n_sensors < 1 ||
@@ -1433,7 +1530,11 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
             k_forward<false, true><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         else
             k_forward<false, false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
-        if (p.nchunk > 1) {
+        if (p.nchunk > 1 && !ac.exact && fwd_cmb()) {
+            k_forward_combine<<<dim3(M, F), 256, 0, st>>>(
+                partial, bounds, array->positions, ac, observed, out,
+                want_loss ? lpart : nullptr, p.nchunk, F, M, T);
+        } else if (p.nchunk > 1) {
             k_forward_finish<<<dim3(M, F), 256, 0, st>>>(
                 partial, observed, out, want_loss ? lpart : nullptr, p.nchunk, F, M, T,
                 finish_vec(partial, observed, out, T));
