@@ -1530,7 +1530,9 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
             k_forward<false, true><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         else
             k_forward<false, false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
-        if (p.nchunk > 1 && !ac.exact && fwd_cmb()) {
+        // the ranged combine pays off on long rows (config 2: -0.7 %; config
+        // 1, T = 2048 with wide ranges: +15 % against the dense float4 path)
+        if (p.nchunk > 1 && !ac.exact && fwd_cmb() && T >= 4096) {
             k_forward_combine<<<dim3(M, F), 256, 0, st>>>(
                 partial, bounds, array->positions, ac, observed, out,
                 want_loss ? lpart : nullptr, p.nchunk, F, M, T);
