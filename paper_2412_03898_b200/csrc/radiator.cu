@@ -222,7 +222,52 @@ struct FwdArgs {
     ArrayConsts ac;
     int Tseg, nseg, nchunk;
     int64_t chunk_balls;
+    // host-precomputed casts / products of ArrayConsts for the per-pair
+    // setup (the same IEEE operations pair_setup performs on the device,
+    // so the setup is bit-identical; ptxas otherwise re-converts them from
+    // the double constants in every batch)
+    float inv_v_f, t0_f, inv_dt_f, sa_f, vt0_f, vdt_f;
+    double vdt_d, vt0_d;
 };
+
+#ifndef PC_FWD_FCONST
+#define PC_FWD_FCONST 1
+#endif
+// pair_setup (common.cuh) with the array constants taken from FwdArgs'
+// precomputed fields; identical arithmetic.
+__device__ __forceinline__ void pair_setup_fwd(double dx, double dy, double dz, float a0,
+                                               const FwdArgs& a, int clip_lo, int clip_hi,
+                                               PairSetup& q, float s) {
+    const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const float r2f = (float)R2;
+    const float rinv = rsqrtf(r2f);
+    const float rf = r2f * rinv;
+    const double R = r2f > 1e-30f
+                         ? fma(fma(-(double)rf, (double)rf, R2), 0.5 * (double)rinv, (double)rf)
+                         : sqrt(R2);
+    q.R = R;
+    int lo, hi;
+    const float tc = ((float)R * a.inv_v_f - a.t0_f) * a.inv_dt_f;
+    const int T = a.ac.T;
+    if (a.ac.exact) {
+        lo = 0;
+        hi = T;
+    } else {
+        const float sa = a.sa_f * a0;
+        const float flo = ceilf(tc - sa);
+        const float fhi = floorf(tc + sa) + 1.f;
+        lo = (int)fminf(fmaxf(flo, 0.f), (float)T);
+        hi = (int)fminf(fmaxf(fhi, 0.f), (float)T);
+    }
+    q.jl = max(lo, clip_lo);
+    q.jh = min(hi, clip_hi);
+    const int rc = __float2int_rn(tc);
+    q.jr = min(max(rc, q.jl), max(q.jh - 1, q.jl));
+    const double vt = fma((double)q.jr, a.vdt_d, a.vt0_d);
+    q.X = (float)(R - vt) * s;
+    q.Y = (float)(R + vt) * s;
+    q.near = (float)R + a.vt0_f + a.vdt_f * (float)q.jl < 10.f * a0;
+}
 
 // Both half-warps sweep the same ball for their own sensor: lane `sub` of a
 // half owns sample pairs (j, j+1), j = je0 + 2 sub + FSTR n, so each half's
@@ -482,8 +527,13 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 const float s = scale_of(av);
                 const size_t q3 = 3 * (fb + i);
                 PairSetup q;
+#if PC_FWD_FCONST
+                pair_setup_fwd(a.mu[q3] - px, a.mu[q3 + 1] - py, a.mu[q3 + 2] - pz, av, a, s0, s1,
+                               q, s);
+#else
                 pair_setup(a.mu[q3] - px, a.mu[q3 + 1] - py, a.mu[q3 + 2] - pz, av, s, a.ac, s0,
                            s1, q);
+#endif
                 if (q.R < kCoincidenceEps) {
                     atomicMin(a.coinc, (long long)i * a.M + m);
                     pass = false;
@@ -1505,6 +1555,14 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         a.nseg = p.nseg;
         a.nchunk = p.nchunk;
         a.chunk_balls = p.chunk_balls;
+        a.inv_v_f = (float)ac.inv_v;
+        a.t0_f = (float)ac.t0;
+        a.inv_dt_f = (float)ac.inv_dt;
+        a.sa_f = (float)(ac.support * ac.inv_v * ac.inv_dt);
+        a.vt0_f = (float)(ac.v * ac.t0);
+        a.vdt_f = (float)(ac.v * ac.dt);
+        a.vdt_d = ac.v * ac.dt;
+        a.vt0_d = ac.v * ac.t0;
         const size_t smem = fwd_smem_bytes(p.Tseg);
         // the dynamic shared-memory opt-in is per device: track it per device
         static unsigned long long attr_set = 0;
