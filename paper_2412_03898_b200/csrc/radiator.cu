@@ -508,13 +508,18 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
     __syncwarp();
 
     if (scan) {
-        float4 nxt = b0 + sub < b1 ? cl[b0 + sub] : make_float4(0.f, 0.f, 0.f, 1.f);
-        for (int64_t g = b0; g < b1; g += FBATCH) {
+        // 32-bit ball offsets within the chunk (chunks hold < 2^31 balls)
+        const int nbc = (int)(b1 - b0);
+        const float4* clc = cl + b0;
+        const double* muc = a.mu + 3 * (fb + b0);
+        const float* p0c = a.p0 + fb + b0;
+        float4 nxt = sub < nbc ? clc[sub] : make_float4(0.f, 0.f, 0.f, 1.f);
+        for (int g = 0; g < nbc; g += FBATCH) {
             const float4 cur = nxt;
-            const int64_t i = g + sub;                  // this lane's ball (sensor h)
-            if (g + FBATCH + sub < b1) nxt = cl[g + FBATCH + sub];
+            const int i = g + sub;                      // this lane's ball (sensor h)
+            if (g + FBATCH + sub < nbc) nxt = clc[g + FBATCH + sub];
             bool pass = false;
-            if (i < b1 && m >= 0) {
+            if (i < nbc && m >= 0) {
                 const float dx = cur.x - fpx, dy = cur.y - fpy, dz = cur.z - fpz;
                 const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                 const float w = sup * cur.w + 1e-5f * r;
@@ -525,22 +530,22 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             if (pass) {
                 const float av = cur.w;
                 const float s = scale_of(av);
-                const size_t q3 = 3 * (fb + i);
+                const int q3 = 3 * i;
                 PairSetup q;
 #if PC_FWD_FCONST
-                pair_setup_fwd(a.mu[q3] - px, a.mu[q3 + 1] - py, a.mu[q3 + 2] - pz, av, a, s0, s1,
+                pair_setup_fwd(muc[q3] - px, muc[q3 + 1] - py, muc[q3 + 2] - pz, av, a, s0, s1,
                                q, s);
 #else
-                pair_setup(a.mu[q3] - px, a.mu[q3 + 1] - py, a.mu[q3 + 2] - pz, av, s, a.ac, s0,
+                pair_setup(muc[q3] - px, muc[q3 + 1] - py, muc[q3 + 2] - pz, av, s, a.ac, s0,
                            s1, q);
 #endif
                 if (q.R < kCoincidenceEps) {
-                    atomicMin(a.coinc, (long long)i * a.M + m);
+                    atomicMin(a.coinc, (long long)(b0 + i) * a.M + m);
                     pass = false;
                 } else if (q.jh <= q.jl) {
                     pass = false;
                 } else {
-                    const float c = __fdividef(0.5f * __ldg(a.p0 + fb + i), (float)q.R * s);
+                    const float c = __fdividef(0.5f * __ldg(p0c + i), (float)q.R * s);
                     const float vs = vdt * s;
                     const int je0 = q.jl & ~1;
                     const int je1 = (q.jh + 1) & ~1;
