@@ -234,6 +234,9 @@ struct FwdArgs {
 // amplitude move by ~2e-7 relative, far inside the 1e-5 signal tolerance;
 // the IEEE division's slow path cost 112 instructions of code and 0.7 % of
 // the forward)
+#ifndef PC_FWD_NOCULL1
+#define PC_FWD_NOCULL1 1
+#endif
 #ifndef PC_FWD_FASTDIV
 #define PC_FWD_FASTDIV 1
 #endif
@@ -531,6 +534,13 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             const int i = g + sub;                      // this lane's ball (sensor h)
             if (g + FBATCH + sub < nbc) nxt = clc[g + FBATCH + sub];
             bool pass = false;
+#if PC_FWD_NOCULL1
+            // one segment holds the whole arrival range of the chunk box: every
+            // ball's window meets it, the cull is skipped
+            if (i < nbc && m >= 0 && nseg_w == 1) {
+                pass = true;
+            } else
+#endif
             if (i < nbc && m >= 0) {
                 const float dx = cur.x - fpx, dy = cur.y - fpy, dz = cur.z - fpz;
                 const float r = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
