@@ -228,6 +228,7 @@ struct FwdArgs {
     // the double constants in every batch)
     float inv_v_f, t0_f, inv_dt_f, sa_f, vt0_f, vdt_f;
     double vdt_d, vt0_d;
+    int part_margin;     // > 0: partial rows written over the active range +- margin only
 };
 
 // s = sqrt(log2 e / 2) / a0 by the approximate division (2 ulp: x and the
@@ -643,7 +644,12 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
         const size_t row = ((size_t)f * a.M + mq) * T;
         if (a.nchunk > 1) {
             float* dst = a.out + (size_t)chunk * a.F * a.M * T + row;
-            for (int j = w0 + lane; j < w1; j += 32) dst[j] = (j >= s0 && j < s1) ? tq[j] : 0.f;
+            // with the ranged combine only the active part (+ a 16-sample
+            // margin of zeros, covering the combine's wider padding) is
+            // written; the dense combine reads whole rows
+            const int p0w = a.part_margin ? max(w0, s0 - a.part_margin) : w0;
+            const int p1w = a.part_margin ? min(w1, s1 + a.part_margin) : w1;
+            for (int j = p0w + lane; j < p1w; j += 32) dst[j] = (j >= s0 && j < s1) ? tq[j] : 0.f;
             continue;
         }
         double lsum = 0.0;
@@ -1507,6 +1513,16 @@ static bool fwd_cmb() {
     return v != 0;
 }
 
+// Partial rows written over the active range only (PC_FWD_PM=0: whole rows).
+static bool fwd_pm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PC_FWD_PM");
+        v = e ? atoi(e) != 0 : 1;
+    }
+    return v != 0;
+}
+
 extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array_t* array,
                                int32_t* plan) {
     if (!array || !plan || n_balls < 0 || n_frames < 1 || array->n_sensors < 1 ||
@@ -1590,6 +1606,8 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         a.vdt_f = (float)(ac.v * ac.dt);
         a.vdt_d = ac.v * ac.dt;
         a.vt0_d = ac.v * ac.t0;
+        const bool ranged = p.nchunk > 1 && !ac.exact && fwd_cmb() && T >= 4096;
+        a.part_margin = ranged && fwd_pm() ? 16 : 0;
         const size_t smem = fwd_smem_bytes(p.Tseg);
         // the dynamic shared-memory opt-in is per device: track it per device
         static unsigned long long attr_set = 0;
@@ -1617,7 +1635,7 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
             k_forward<false, false><<<grid, FWD_WARPS * 32, smem, st>>>(a);
         // the ranged combine pays off on long rows (config 2: -0.7 %; config
         // 1, T = 2048 with wide ranges: +15 % against the dense float4 path)
-        if (p.nchunk > 1 && !ac.exact && fwd_cmb() && T >= 4096) {
+        if (ranged) {
             k_forward_combine<<<dim3(M, F), 256, 0, st>>>(
                 partial, bounds, array->positions, ac, observed, out,
                 want_loss ? lpart : nullptr, p.nchunk, F, M, T);
