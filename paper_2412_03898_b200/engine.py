@@ -193,6 +193,8 @@ class IterationEngine:
         self._status_host = None
         self._status_dev = None
         self._bufs_F = -1
+        self.mu_t = None
+        self.ws = None
         n_seg = len(self.layout.segments)
         self.flags = torch.zeros(n_seg, dtype=torch.int32, device=self.device)
         self.coinc = torch.full((1,), _lib.INT64_MAX, dtype=torch.int64,
@@ -230,21 +232,26 @@ class IterationEngine:
 
     # ------------------------------------------------------------ buffers
     def _ensure_buffers(self, F: int):
-        if self._bufs_F == F and self.mu_t.shape[1] == self.B:
+        if (self._bufs_F == F and self.mu_t is not None
+                and self.mu_t.shape[1] == self.B):
             return
         dev, B, M, T = self.device, self.B, self.darr.M, self.darr.T
-        self.t_dev = torch.zeros(F, dtype=torch.float64, device=dev)
+        if self._bufs_F != F:
+            # per-frame buffers that do not depend on the ball count (kept
+            # across densify steps: the residual alone is F*M*T floats)
+            self.t_dev = torch.zeros(F, dtype=torch.float64, device=dev)
+            self.resid = torch.empty((F, M, T), dtype=torch.float32, device=dev)
+            self.loss_f = torch.zeros(F, dtype=torch.float64, device=dev)
+            self.obs_stage = None
+            self.loss_part = torch.empty(F * M, dtype=torch.float64, device=dev)
         self.mu_t = torch.empty((F, B, 3), dtype=torch.float64, device=dev)
         self.a0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
         self.p0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
         self.H = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
-        self.resid = torch.empty((F, M, T), dtype=torch.float32, device=dev)
         self.G = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
-        self.loss_f = torch.zeros(F, dtype=torch.float64, device=dev)
         ws = self.darr.workspace_bytes(max(B, 1), F)
-        self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
-        self.obs_stage = None
-        self.loss_part = torch.empty(F * M, dtype=torch.float64, device=dev)
+        if self.ws is None or self.ws.numel() < ws:
+            self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
         self._bufs_F = F
         self._graph = None
 
@@ -674,8 +681,7 @@ class IterationEngine:
                                   p.get("sigma"), p["omega"], self.basis)
         self.order = np.arange(B2, dtype=np.int64)
         self.inverse = self.order.copy()
-        self._bufs_F = -1
-        self._graph = None
+        self._graph = None          # B changed: _ensure_buffers re-sizes the ball buffers
         return B - n_keep, n_split
 
     # ------------------------------------------------------------ views
