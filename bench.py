@@ -339,7 +339,9 @@ def run_ours(args, rank, world, local):
         barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     if os.environ.get("PC_BENCH_DEBUG"):
-        print("step ms", [round(x, 3) for x in step_ms], "B", eng.B, file=sys.stderr)
+        print("step ms", [round(x, 3) for x in step_ms], "B", eng.B,
+              "mem MB", torch.cuda.memory_allocated() >> 20,
+              "peak MB", torch.cuda.max_memory_allocated() >> 20, file=sys.stderr)
     ms = float(np.mean(step_ms))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)

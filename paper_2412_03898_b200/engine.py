@@ -190,6 +190,7 @@ class IterationEngine:
         self._tail_graph = None
         self._tail_key = None
         self._tail_warmed = False
+        self._pool = None
         self._status_host = None
         self._status_dev = None
         self._bufs_F = -1
@@ -251,7 +252,10 @@ class IterationEngine:
         self.G = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
         ws = self.darr.workspace_bytes(max(B, 1), F)
         if self.ws is None or self.ws.numel() < ws:
-            self.ws = torch.empty(max(ws, 1), dtype=torch.uint8, device=dev)
+            # 25 % headroom: a growing cloud (densify) re-allocates the
+            # workspace (chunk partial traces, ~GBs) rarely
+            self.ws = None
+            self.ws = torch.empty(max(ws + ws // 4, 1), dtype=torch.uint8, device=dev)
         self._bufs_F = F
         self._graph = None
 
@@ -365,18 +369,33 @@ class IterationEngine:
             if not self._warmed:
                 self._launch_compute(obs, host_src)
                 self._warmed = True
-            g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream(device=self.device)
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    self._launch_compute(obs, host_src)
-            torch.cuda.current_stream().wait_stream(s)
+            self._graph = None
+            g = self._capture(lambda: self._launch_compute(obs, host_src))
             self._graph, self._graph_frames = g, key
             self._graph.replay()
         else:
             self._graph = None      # t_dev / obs changed under the graph
             self._launch_compute(obs, host_src)
+
+    def _capture(self, launch):
+        """Capture `launch` into a CUDA graph on a side stream, in this
+        engine's own memory pool.  CUDAGraph.capture_begin/capture_end
+        directly: the torch.cuda.graph context manager also runs
+        gc.collect() and torch.cuda.empty_cache() before every capture,
+        which stalled the re-capture after a densify step for up to 1 s."""
+        if self._pool is None:
+            self._pool = torch.cuda.graph_pool_handle()
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream(device=self.device)
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            g.capture_begin(pool=self._pool)
+            try:
+                launch()
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream().wait_stream(st)
+        return g
 
     def allreduce(self) -> None:
         if self.world > 1:
@@ -529,13 +548,8 @@ class IterationEngine:
             self._launch_tail()          # eager once (lazy library init)
             self._tail_warmed = True
             return
-        g = torch.cuda.CUDAGraph()
-        st = torch.cuda.Stream(device=self.device)
-        st.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(st):
-            with torch.cuda.graph(g, stream=st):
-                self._launch_tail()
-        torch.cuda.current_stream().wait_stream(st)
+        self._tail_graph = None
+        g = self._capture(self._launch_tail)
         self._tail_graph, self._tail_key = g, key
         g.replay()
 
