@@ -47,7 +47,10 @@ constexpr int64_t FWD_CHUNK_BALLS = 16384;            // balls per forward chunk
 #define PC_FWD_MIN_CHUNK 128
 #endif
 constexpr int64_t FWD_MIN_CHUNK_BALLS = PC_FWD_MIN_CHUNK; // balls per forward chunk (min)
-constexpr size_t FWD_PARTIAL_BUDGET = (size_t)16 << 30;  // bytes of chunk partial traces
+#ifndef PC_FWD_BUDGET_GB
+#define PC_FWD_BUDGET_GB 48
+#endif
+constexpr size_t FWD_PARTIAL_BUDGET = (size_t)PC_FWD_BUDGET_GB << 30;  // bytes of chunk partial traces
 constexpr int TRACE_PAD = 8;        // floats after a trace (even-window overrun)
 
 struct FwdPlan {
