@@ -613,7 +613,6 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
             }
             // compact: balls with a live pair for either sensor, in batch order
             const unsigned pm = __ballot_sync(0xffffffffu, pass);
-            const bool anyslow = __any_sync(0xffffffffu, slow);
             unsigned bm = pm;
 #pragma unroll
             for (int o = FL; o < 32; o <<= 1) bm |= bm >> o;
@@ -630,7 +629,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                 const int w = __float_as_int(r0.x);
                 if (w < 0)
                     fwd_sweep_recur(lbase, r0, recs[k].r1, 2 * sub, subq);
-                else if (EXACT || (anyslow && ((w >> 30) & 1)))
+                else if (EXACT || ((w >> 30) & 1))
                     fwd_sweep_slow(lbase, r0, recs[k].r1, sub2, 2 * sub);
                 else
                     fwd_sweep_fast(lbase, r0, recs[k].r1, 2 * sub, subq);
