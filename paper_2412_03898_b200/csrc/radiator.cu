@@ -18,17 +18,20 @@ namespace pc {
 
 // ---------------------------------------------------------------- forward
 //
-// CTA = FWD_WARPS sensors x one time segment x one frame (x one ball chunk).
-// Each warp owns one sensor's segment as a private shared-memory trace, so
+// CTA = FWD_WARPS warps x FSW (2) sensors x one time segment x one frame x
+// one ball chunk.  Each sensor has a private shared-memory trace, so
 // accumulation needs no atomics and its order is fixed (deterministic).
-// Warps never synchronise with each other: each streams the frame's ball
+// Warps never synchronise with each other: each streams the chunk's ball
 // records (a compact float4 {x, y, z, a0} cull record, L1/L2 resident) with a
-// one-group prefetch.  Segments are laid over the sensor's ACTIVE arrival
-// range, derived from the frame's ball bounding box, so no segment is empty.
-// Per 32-ball group a lane-parallel fp32 cull drops balls whose +-6 sigma
-// window misses the segment; surviving pairs get the fp64 setup and a 32-byte
-// record; then the warp sweeps each surviving ball's window, lanes on
-// consecutive samples.
+// one-batch prefetch.  Segments are laid over the warp's ACTIVE arrival range,
+// derived from the (frame, chunk) ball bounding box, so no segment is empty.
+// Per 16-ball batch a lane-parallel fp32 cull (skipped when one segment holds
+// the whole range) drops balls whose +-6 sigma window misses the segment;
+// surviving pairs get the fp64 setup and a 32-byte record; then both
+// half-warps sweep each surviving ball's window for their own sensor, lanes
+// on consecutive sample pairs.  With ball chunks, each chunk's partial traces
+// are written over the active range and combined in fixed chunk order by
+// k_forward_combine (k_forward_finish for dense rows).
 
 #ifndef PC_FWD_WARPS
 #define PC_FWD_WARPS 4
