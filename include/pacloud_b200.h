@@ -55,11 +55,20 @@ typedef struct pc_array {
     double dt;               /* us, 1/sample_rate (core.py:345-347) */
     double support_sigmas;   /* radiator.py:31 DEFAULT_SUPPORT_SIGMAS */
     int32_t exact;           /* evaluate every sample (radiator.py:100-102) */
-    int32_t reserved;
+    int32_t sensor_offset;   /* global index of local sensor 0 (sensor
+                                sharding; 0 for a whole array) */
     const int32_t *sensor_order; /* device, (M,) processing order of the
                                     sensors (spatially clustered) or NULL;
                                     outputs stay in sensor index order */
+    int32_t n_sensors_total; /* sensors of the whole array (0 = n_sensors) */
+    int32_t frame_offset;    /* global position of local frame 0 in the
+                                iteration's frame list (frame sharding) */
 } pc_array_t;
+
+/* Coincidence word (radiator.py:97-99): the kernels atomicMin
+ *   ((frame_offset + f) * B + b) * n_sensors_total + sensor_offset + m
+ * over every pair (f, b, m) with R < 1e-9 into a device int64 that holds
+ * INT64_MAX on entry; one frame of a whole array gives b * M + m. */
 
 /* DynamicCloud (core.py:166-259), device f64 arrays.
  * Gaussian basis: theta/sigma (B,N) shared or (B,5,N) per-channel.
@@ -92,12 +101,22 @@ typedef struct pc_cloud_grads {
 
 /* Replaces deformation.py:184-204 cloud_states_at, batched over F frames
  * (the reference calls it once per frame, reconstruction.py:305).
- * a0_floor <= 0 disables the clamp (a0_floor=None).  H (F,B,5) f32 receives
- * the channel sums for pc_deform_backward (may be NULL). */
+ * a0_floor NaN disables the clamp (a0_floor=None); any other value clamps
+ * a0_t = max(a0 (1 + H0), a0_floor) as deformation.py:202-203 does.  H
+ * (F,B,5) f32 receives the channel sums for pc_deform_backward (may be
+ * NULL), with H[...,0] = NaN where the floor clamped (the backward's
+ * subgradient flag, deformation.py:257-264, decided here in fp64). */
 int pc_deform_states(const pc_cloud_t *cloud, const double *t_frames_dev,
                      int32_t n_frames, int32_t coord_mode, double a0_floor,
                      double *mu_t, float *a0_t, float *p0_t, float *H,
                      pc_stream_t stream);
+
+/* pc_deform_states with float64 a0_t / p0_t (the drop-in cloud_states_at
+ * returns the reference's float64 CloudState, deformation.py:31-54). */
+int pc_deform_states_f64(const pc_cloud_t *cloud, const double *t_frames_dev,
+                         int32_t n_frames, int32_t coord_mode, double a0_floor,
+                         double *mu_t, double *a0_t, double *p0_t,
+                         pc_stream_t stream);
 
 /* Replaces deformation.py:219-267 cloud_state_grads at one frame time
  * (materialised Jacobians, f64; API compatibility -- the fused engine never
@@ -105,6 +124,16 @@ int pc_deform_states(const pc_cloud_t *cloud, const double *t_frames_dev,
 int pc_deform_jacobian(const pc_cloud_t *cloud, double t, int32_t coord_mode,
                        double a0_floor, double *d_base, double *d_omega,
                        double *d_theta, double *d_sigma, pc_stream_t stream);
+
+/* Replaces deformation.py:57-70 eval_basis: out[i] = exp(-(t - theta)^2 /
+ * (2 sigma^2)) over n already-broadcast device fp64 values. */
+int pc_eval_basis(const double *t, const double *theta, const double *sigma,
+                  int64_t n, double *out, pc_stream_t stream);
+
+/* Replaces deformation.py:73-84 eval_H: out[0] = sum_n omega[n] *
+ * eval_basis(t, theta[n], sigma[n]) (index order, fp64; device arrays). */
+int pc_eval_h(double t, const double *omega, const double *theta,
+              const double *sigma, int32_t n, double *out, pc_stream_t stream);
 
 /* Replaces radiator.py:278-294 (accumulate_frame_grads' chain rule) for one
  * frame: G (B,5) f32 through a materialised Jacobian bundle into f64 grads.
@@ -145,7 +174,8 @@ size_t pc_forward_workspace_bytes(int64_t n_balls, int32_t n_frames,
  * receives predicted - observed and loss_per_frame[f] = 0.5*sum r^2 (f64);
  * otherwise `out` receives the predicted traces.  `out` is overwritten.
  * coincident: device int64, must hold INT64_MAX on entry; receives the
- * smallest b*M+m of any pair with R < 1e-9 (radiator.py:97-99). */
+ * smallest coincidence word (see pc_array_t) of any pair with R < 1e-9
+ * (radiator.py:97-99). */
 int pc_forward_traces(const double *mu_t, const float *a0_t,
                       const float *p0_t, int64_t n_balls, int32_t n_frames,
                       const pc_array_t *array, const float *observed,
@@ -172,6 +202,16 @@ int pc_residual_state_grads(const double *mu_t, const float *a0_t,
                             int32_t n_frames, const pc_array_t *array,
                             const float *residual, float *G,
                             int64_t *coincident, pc_stream_t stream);
+
+/* Replaces radiator.py:36-55 pressure_kernel (out) and :58-83
+ * pressure_kernel_grad (d_p0, d_a0, d_R; all three or none), elementwise in
+ * fp64 over n already-broadcast device values of R, t, p0, a0 (sound speed
+ * v > 0).  Input validation (R > 0, a0 > 0) is the caller's, as the
+ * reference raises before evaluating. */
+int pc_pressure_kernel(const double *R, const double *t, const double *p0,
+                       const double *a0, int64_t n, double sound_speed,
+                       double *out, double *d_p0, double *d_a0, double *d_R,
+                       pc_stream_t stream);
 
 /* ---- evaluation --------------------------------------------------------- */
 
@@ -219,6 +259,18 @@ int pc_l2_loss(const double *predicted, const double *observed, int64_t n,
 int pc_check_finite(const float *x, int32_t n_seg, const int64_t *seg_off,
                     int32_t *flags, pc_stream_t stream);
 
+/* float64-gradient variants (the drop-in adam_step / sgd_step take the
+ * caller's float64 gradient, reconstruction.py:57-76). */
+int pc_check_finite_f64(const double *x, int32_t n_seg, const int64_t *seg_off,
+                        int32_t *flags, pc_stream_t stream);
+int pc_adam_segments_f64(double *params, const double *grads, double *m,
+                         double *v, int32_t n_seg, const int64_t *seg_off,
+                         const double *seg_lr, const int32_t *seg_step,
+                         const double *seg_floor, pc_stream_t stream);
+int pc_sgd_segments_f64(double *params, const double *grads, int32_t n_seg,
+                        const int64_t *seg_off, const double *seg_lr,
+                        const double *seg_floor, pc_stream_t stream);
+
 /* Replaces reconstruction.py:57-69 adam_step (+ the floors of :153-157) for
  * n_seg parameter segments of one flat buffer in one launch.  Per segment:
  * learning rate, step count t (after increment) and lower floor
@@ -236,10 +288,14 @@ int pc_adam_segments(double *params, const float *grads, double *m,
  * and the reference's guard semantics decided on the device: nothing is
  * updated if *coincident_dev != INT64_MAX or *loss_dev is not finite
  * (radiator.py:186-192, reconstruction.py:317-318); otherwise the segments
- * whose group (seg_group, host, in update order) precedes the first group
- * with a non-finite flag (flags_dev, from pc_check_finite) are updated
- * (reconstruction.py:60-61, 320-327).  seg_off / seg_floor / seg_group are
- * host arrays. */
+ * (one per parameter array, in the reference's update order: pressure, std,
+ * coords, then deform's theta, sigma, omega) before the first segment with a
+ * non-finite flag (flags_dev, from pc_check_finite) are updated -- adam_step
+ * raises per ARRAY before touching it (reconstruction.py:60-61, 88-93,
+ * 320-327) -- and the floors (seg_floor) apply only when every segment was
+ * stepped (the raise skips _clamp_floors, :328).  seg_group (host, the
+ * segment's group index) is kept for the caller's bookkeeping.  seg_off /
+ * seg_floor / seg_group are host arrays. */
 int pc_update_guarded(double *params, const float *grads, double *m,
                       double *v, int32_t n_seg, const int64_t *seg_off,
                       const double *seg_floor, const int32_t *seg_group,

@@ -4,8 +4,10 @@ Drop-in replacements for the reference ``pacloud`` hot-path calls, backed by
 hand-written sm_100a CUDA kernels behind a C ABI (libpacloud_b200.so,
 include/pacloud_b200.h):
 
-    deformation.cloud_states_at / cloud_state_grads
-    radiator.forward_frame / frame_state_grads / accumulate_frame_grads
+    deformation.cloud_states_at / cloud_state_grads / ball_state_at /
+        ball_state_grad / eval_basis / eval_H
+    radiator.forward_frame / frame_state_grads / accumulate_frame_grads /
+        pressure_kernel / pressure_kernel_grad
     reconstruction.l2_loss / adam_step / sgd_step / ParamGroup(s) /
         dynamic_reconstruct
     engine.IterationEngine      fused multi-frame iteration (+ NCCL sharding)
@@ -18,18 +20,21 @@ include/pacloud_b200.h):
 """
 
 from .core import (AdamState, BallStateAtT, Box, CloudGrads, CloudState,
-                   GaussBall,
+                   GaussBall, DeformField, Violation, validate_cloud,
                    CloudStateGrad, DynamicCloud, ReconConfig, SensorArray,
                    SignalSet, VoxelGrid, default_basis_grid, frame_times)
-from .deformation import cloud_state_grads, cloud_states_at
+from .deformation import (BallStateGrad, ball_state_at, ball_state_grad,
+                          cloud_state_grads, cloud_states_at, eval_basis,
+                          eval_H)
 from .engine import IterationEngine
 from .evaluation import (GridSpec, eval_report, format_report, map_project,
                          ssim, voxelize)
 from .fileio import read_cloud, read_tensor, write_cloud, write_tensor
 from .geometry import (Phantom, PhantomSpec, build_phantom, fibonacci_sphere,
                        simulate_dataset, spherical_array)
-from .radiator import (accumulate_frame_grads, forward_frame,
-                       frame_state_grads)
+from .radiator import (accumulate_frame_grads, compute_time_window,
+                       forward_frame, frame_state_grads, pressure_kernel,
+                       pressure_kernel_grad)
 from .reconstruction import (ParamGroup, ParamGroups, adam_step,
                              dynamic_reconstruct, l2_loss, scheduled_lr,
                              sgd_step)
@@ -50,4 +55,7 @@ __all__ = [
     "build_phantom", "fibonacci_sphere", "simulate_dataset", "spherical_array",
     "read_cloud", "read_tensor", "write_cloud", "write_tensor",
     "static_reconstruct", "GaussBall", "ubp_reconstruct",
+    "DeformField", "Violation", "validate_cloud", "BallStateGrad",
+    "ball_state_at", "ball_state_grad", "eval_basis", "eval_H",
+    "compute_time_window", "pressure_kernel", "pressure_kernel_grad",
 ]

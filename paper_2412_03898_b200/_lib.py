@@ -30,7 +30,8 @@ class PcArray(Structure):
                 ("n_samples", c_int32), ("sound_speed", c_double),
                 ("t_start", c_double), ("dt", c_double),
                 ("support_sigmas", c_double), ("exact", c_int32),
-                ("reserved", c_int32), ("sensor_order", c_void_p)]
+                ("sensor_offset", c_int32), ("sensor_order", c_void_p),
+                ("n_sensors_total", c_int32), ("frame_offset", c_int32)]
 
 
 class PcCloud(Structure):
@@ -52,6 +53,10 @@ _P = c_void_p
 SIGNATURES = {
     "pc_deform_states": (c_int32, [POINTER(PcCloud), _P, c_int32, c_int32,
                                    c_double, _P, _P, _P, _P, _P]),
+    "pc_deform_states_f64": (c_int32, [POINTER(PcCloud), _P, c_int32,
+                                       c_int32, c_double, _P, _P, _P, _P]),
+    "pc_eval_basis": (c_int32, [_P, _P, _P, c_int64, _P, _P]),
+    "pc_eval_h": (c_int32, [c_double, _P, _P, _P, c_int32, _P, _P]),
     "pc_deform_jacobian": (c_int32, [POINTER(PcCloud), c_double, c_int32,
                                      c_double, _P, _P, _P, _P, _P]),
     "pc_assemble_grads": (c_int32, [_P, c_int64, c_int32, _P, _P, _P, _P,
@@ -71,6 +76,8 @@ SIGNATURES = {
                                           POINTER(PcArray), _P, _P, _P, _P]),
     "pc_residual_loss": (c_int32, [_P, _P, _P, _P, _P, c_int32, c_int32,
                                    c_int32, _P]),
+    "pc_pressure_kernel": (c_int32, [_P, _P, _P, _P, c_int64, c_double, _P,
+                                     _P, _P, _P, _P]),
     "pc_voxelize_workspace_bytes": (c_size_t, [c_int64]),
     "pc_voxelize": (c_int32, [_P, _P, _P, c_int64, POINTER(c_double),
                               c_double, POINTER(c_int32), c_double, c_int32,
@@ -90,6 +97,15 @@ SIGNATURES = {
                                    POINTER(c_double), _P]),
     "pc_sgd_segments": (c_int32, [_P, _P, c_int32, POINTER(c_int64),
                                   POINTER(c_double), POINTER(c_double), _P]),
+    "pc_check_finite_f64": (c_int32, [_P, c_int32, POINTER(c_int64), _P,
+                                      _P]),
+    "pc_adam_segments_f64": (c_int32, [_P, _P, _P, _P, c_int32,
+                                       POINTER(c_int64), POINTER(c_double),
+                                       POINTER(c_int32), POINTER(c_double),
+                                       _P]),
+    "pc_sgd_segments_f64": (c_int32, [_P, _P, c_int32, POINTER(c_int64),
+                                      POINTER(c_double), POINTER(c_double),
+                                      _P]),
     "pc_compact_workspace_bytes": (c_size_t, [c_int64]),
     "pc_prune_mask": (c_int32, [_P, c_int64, c_double, _P, _P, _P, c_size_t,
                                 _P]),

@@ -129,6 +129,78 @@ class GaussBall:
 
 
 @dataclass(frozen=True)
+class DeformField:
+    """Gaussian-basis temporal deformation curves for one ball (reference
+    core.py:105-135): theta / sigma shared (N,) or per-channel (5, N),
+    omega (5, N)."""
+
+    theta: np.ndarray
+    sigma: np.ndarray
+    omega: np.ndarray
+
+    def __post_init__(self):
+        theta = np.asarray(self.theta, dtype=np.float64)
+        sigma = np.asarray(self.sigma, dtype=np.float64)
+        omega = np.asarray(self.omega, dtype=np.float64)
+        if theta.ndim not in (1, 2) or theta.shape != sigma.shape:
+            raise ValueError("theta and sigma must share shape (N,) or (5, N)")
+        if theta.ndim == 2 and theta.shape[0] != N_CHANNELS:
+            raise ValueError(f"per-channel theta must have {N_CHANNELS} rows")
+        n = theta.shape[-1]
+        if omega.shape != (N_CHANNELS, n):
+            raise ValueError(
+                f"omega must have shape ({N_CHANNELS}, {n}), got {omega.shape}")
+        if np.any(sigma <= 0):
+            raise ValueError("all basis widths sigma must be > 0")
+        object.__setattr__(self, "theta", theta)
+        object.__setattr__(self, "sigma", sigma)
+        object.__setattr__(self, "omega", omega)
+
+    @property
+    def n_basis(self) -> int:
+        return int(self.theta.shape[-1])
+
+    @property
+    def shared_basis(self) -> bool:
+        return self.theta.ndim == 1
+
+
+@dataclass(frozen=True)
+class Violation:
+    """One invariant violation found by `validate_cloud` (core.py:262-268)."""
+
+    index: int
+    field: str
+    message: str
+
+
+def validate_cloud(cloud, roi) -> list:
+    """Diagnostic scan of a cloud against the type invariants and an ROI
+    (reference core.py:271-292): a0 > 0, p0 >= 0, basis widths > 0, centres
+    inside `roi` (inclusive).  Never raises.  Host-side bookkeeping over the
+    caller's arrays, as in the reference."""
+    out = []
+    p0 = np.asarray(cloud.p0, dtype=np.float64)
+    a0 = np.asarray(cloud.a0, dtype=np.float64)
+    mu = np.asarray(cloud.mu, dtype=np.float64).reshape(-1, 3)
+    sigma = getattr(cloud, "sigma", None)
+    sigma = None if sigma is None else np.asarray(sigma, dtype=np.float64)
+    n = len(p0)
+    inside = roi.contains(mu) if n else np.zeros(0, bool)
+    for i in range(n):
+        if not a0[i] > 0:
+            out.append(Violation(i, "a0", f"a0 = {a0[i]} is not > 0"))
+        if p0[i] < 0:
+            out.append(Violation(i, "p0", f"p0 = {p0[i]} is negative"))
+        if sigma is not None and np.any(sigma[i] <= 0):
+            out.append(Violation(i, "sigma", "basis width <= 0"))
+        if not inside[i]:
+            out.append(Violation(
+                i, "mu", f"center {mu[i]} outside roi [{roi.lo}, {roi.hi}]"))
+    return out
+
+
+@dataclass(frozen=True)
 class SensorArray:
     """Detector positions plus acoustic and sampling parameters."""
 
@@ -401,6 +473,8 @@ class ReconConfig:
                 raise ValueError(f"{name} must be > 0")
         if self.p0_floor < 0:
             raise ValueError("p0_floor must be >= 0")
+        if self.prune_every < 1 or self.static_iters < 1 or self.dynamic_iters < 1:
+            raise ValueError("iteration counts and prune cadence must be >= 1")
         if self.basis not in BASES:
             raise ValueError(f"basis must be one of {BASES}")
 

@@ -99,11 +99,16 @@ __device__ void channel_sums(const CloudView& c, int64_t b, double t, double H[5
     }
 }
 
+// a0_floor NaN = no floor (a0_floor=None): x < NaN is false, so every
+// non-NaN floor clamps exactly as deformation.py:202-203 (np.maximum).
+// Hout[...,0] = NaN marks a clamped (frame, ball) for pc_deform_backward
+// (the decision is taken here, in fp64).
+template <typename ST>
 __global__ void __launch_bounds__(128) k_deform_states(CloudView c, const double* __restrict__ tf,
                                                        int F, int mode, double a0_floor,
                                                        double* __restrict__ mu_t,
-                                                       float* __restrict__ a0_t,
-                                                       float* __restrict__ p0_t,
+                                                       ST* __restrict__ a0_t,
+                                                       ST* __restrict__ p0_t,
                                                        float* __restrict__ Hout) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= c.B * F) return;
@@ -111,8 +116,9 @@ __global__ void __launch_bounds__(128) k_deform_states(CloudView c, const double
     const int f = (int)(idx - b * F);
     double H[5];
     channel_sums(c, b, tf[f], H);
-    double a0 = c.a0[b] * (1.0 + H[0]);
-    if (a0_floor > 0.0) a0 = fmax(a0, a0_floor);
+    const double a0raw = c.a0[b] * (1.0 + H[0]);
+    const bool clamped = a0raw < a0_floor;
+    const double a0 = clamped ? a0_floor : a0raw;
     const double p0 = c.p0[b] * (1.0 + H[1]);
     const size_t s = (size_t)f * c.B + b;
     for (int k = 0; k < 3; ++k) {
@@ -120,10 +126,11 @@ __global__ void __launch_bounds__(128) k_deform_states(CloudView c, const double
         const double h = H[mode == PC_COORD_RADIAL ? 2 : 2 + k];
         mu_t[3 * s + k] = mode == PC_COORD_ADDITIVE ? mu + h : mu * (1.0 + h);
     }
-    a0_t[s] = (float)a0;
-    p0_t[s] = (float)p0;
+    a0_t[s] = (ST)a0;
+    p0_t[s] = (ST)p0;
     if (Hout) {
         for (int k = 0; k < 5; ++k) Hout[5 * s + k] = (float)H[k];
+        if (clamped) Hout[5 * s] = __int_as_float(0x7fc00000);
     }
 }
 
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(128) k_deform_jacobian(CloudView c, double t, 
     } else {
         for (int s = 0; s < 5; ++s) db[s] = 1.0 + H[rows[s]];
     }
-    const bool clamped = a0_floor > 0.0 && c.a0[b] * (1.0 + H[0]) < a0_floor;
+    const bool clamped = c.a0[b] * (1.0 + H[0]) < a0_floor;   // strict; NaN floor: none
     if (clamped) db[0] = 0.0;
     for (int s = 0; s < 5; ++s) d_base[5 * b + s] = db[s];
     const double* om = c.omega + (size_t)b * 5 * N;
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(128) k_deform_backward(CloudView c, const doub
             Gs[s] = (double)G[s5 + s];
             H[s] = (double)Hs[s5 + s];
         }
-        const bool clamped = a0_floor > 0.0 && a0 * (1.0 + H[0]) < a0_floor;
+        const bool clamped = isnan(H[0]);   // decided in fp64 by k_deform_states
         double db[5];
         if (mode == PC_COORD_ADDITIVE) {
             db[0] = 1.0 + H[0];
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(128) k_deform_backward_pf(CloudView c,
             Gs[s] = (double)G[s5 + s];
             H[s] = (double)Hs[s5 + s];
         }
-        const bool clamped = a0_floor > 0.0 && a0 * (1.0 + H[0]) < a0_floor;
+        const bool clamped = isnan(H[0]);   // decided in fp64 by k_deform_states
         double db[5];
         if (mode == PC_COORD_ADDITIVE) {
             db[0] = 1.0 + H[0];
@@ -429,8 +436,23 @@ extern "C" int pc_deform_states(const pc_cloud_t* cloud, const double* t_frames_
     if (c.B == 0) return PC_OK;
     if (!t_frames_dev || !mu_t || !a0_t || !p0_t) return PC_ERR_ARGUMENT;
     const int64_t n = c.B * n_frames;
-    k_deform_states<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
+    k_deform_states<float><<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
         c, t_frames_dev, n_frames, coord_mode, a0_floor, mu_t, a0_t, p0_t, H);
+    return last_status();
+}
+
+extern "C" int pc_deform_states_f64(const pc_cloud_t* cloud, const double* t_frames_dev,
+                                    int32_t n_frames, int32_t coord_mode, double a0_floor,
+                                    double* mu_t, double* a0_t, double* p0_t,
+                                    pc_stream_t stream) {
+    CloudView c;
+    if (!view_of(cloud, c) || n_frames < 1 || coord_mode < 0 || coord_mode > 2)
+        return PC_ERR_ARGUMENT;
+    if (c.B == 0) return PC_OK;
+    if (!t_frames_dev || !mu_t || !a0_t || !p0_t) return PC_ERR_ARGUMENT;
+    const int64_t n = c.B * n_frames;
+    k_deform_states<double><<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(
+        c, t_frames_dev, n_frames, coord_mode, a0_floor, mu_t, a0_t, p0_t, nullptr);
     return last_status();
 }
 
@@ -498,5 +520,50 @@ extern "C" int pc_deform_backward(const pc_cloud_t* cloud, const double* t_frame
         launch_bwd<true>(ns, blocks, st, c, t_frames_dev, n_frames, coord_mode, a0_floor, G, H, g);
     else
         launch_bwd<false>(ns, blocks, st, c, t_frames_dev, n_frames, coord_mode, a0_floor, G, H, g);
+    return last_status();
+}
+
+// ---------------------------------------------------------------- basis helpers
+//
+// deformation.py:57-70 eval_basis: exp(-(t - theta)^2 / (2 sigma^2)),
+// elementwise over already-broadcast fp64 inputs; and :73-84 eval_H's
+// weighted sum over one basis vector, in index order by one thread.
+__global__ void __launch_bounds__(256) k_eval_basis(const double* __restrict__ t,
+                                                    const double* __restrict__ theta,
+                                                    const double* __restrict__ sigma, int64_t n,
+                                                    double* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = (t[i] - theta[i]) / sigma[i];
+        out[i] = exp(-0.5 * d * d);
+    }
+}
+
+__global__ void k_basis_dot(double t, const double* __restrict__ omega,
+                            const double* __restrict__ theta, const double* __restrict__ sigma,
+                            int n, double* __restrict__ out) {
+    double h = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double d = (t - theta[i]) / sigma[i];
+        h = fma(omega[i], exp(-0.5 * d * d), h);
+    }
+    out[0] = h;
+}
+
+extern "C" int pc_eval_basis(const double* t, const double* theta, const double* sigma,
+                             int64_t n, double* out, pc_stream_t stream) {
+    if (n < 0) return PC_ERR_ARGUMENT;
+    if (n == 0) return PC_OK;
+    if (!t || !theta || !sigma || !out) return PC_ERR_ARGUMENT;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    k_eval_basis<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(t, theta, sigma, n, out);
+    return last_status();
+}
+
+extern "C" int pc_eval_h(double t, const double* omega, const double* theta, const double* sigma,
+                         int32_t n, double* out, pc_stream_t stream) {
+    if (n < 0 || !out || (n > 0 && (!omega || !theta || !sigma))) return PC_ERR_ARGUMENT;
+    k_basis_dot<<<1, 1, 0, as_stream(stream)>>>(t, omega, theta, sigma, n, out);
     return last_status();
 }

@@ -46,7 +46,8 @@ struct SegTable {
     int n;
 };
 
-__global__ void __launch_bounds__(256) k_finite(const float* __restrict__ x, SegTable t,
+template <typename GT>
+__global__ void __launch_bounds__(256) k_finite(const GT* __restrict__ x, SegTable t,
                                                 int* __restrict__ flags) {
     const int s = blockIdx.y;
     const int64_t lo = t.off[s], hi = t.off[s + 1];
@@ -60,7 +61,8 @@ __global__ void __launch_bounds__(256) k_finite(const float* __restrict__ x, Seg
 
 constexpr double kBeta1 = 0.9, kBeta2 = 0.999, kEps = 1e-8;  // reconstruction.py:23-25
 
-__global__ void __launch_bounds__(256) k_adam(double* __restrict__ p, const float* __restrict__ g,
+template <typename GT>
+__global__ void __launch_bounds__(256) k_adam(double* __restrict__ p, const GT* __restrict__ g,
                                               double* __restrict__ m, double* __restrict__ v,
                                               SegTable t) {
     const int s = blockIdx.y;
@@ -82,7 +84,8 @@ __global__ void __launch_bounds__(256) k_adam(double* __restrict__ p, const floa
     }
 }
 
-__global__ void __launch_bounds__(256) k_sgd(double* __restrict__ p, const float* __restrict__ g,
+template <typename GT>
+__global__ void __launch_bounds__(256) k_sgd(double* __restrict__ p, const GT* __restrict__ g,
                                              SegTable t) {
     const int s = blockIdx.y;
     const int64_t lo = t.off[s], hi = t.off[s + 1];
@@ -342,19 +345,30 @@ extern "C" int pc_l2_loss(const double* predicted, const double* observed, int64
     return last_status();
 }
 
-extern "C" int pc_check_finite(const float* x, int32_t n_seg, const int64_t* seg_off,
-                               int32_t* flags, pc_stream_t stream) {
+template <typename GT>
+static int check_finite_impl(const GT* x, int32_t n_seg, const int64_t* seg_off, int32_t* flags,
+                             pc_stream_t stream) {
     SegTable t;
     if (!seg_table(n_seg, seg_off, t) || !flags) return PC_ERR_ARGUMENT;
     if (t.off[n_seg] > t.off[0] && !x) return PC_ERR_ARGUMENT;
-    k_finite<<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(x, t, flags);
+    k_finite<GT><<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(x, t, flags);
     return last_status();
 }
 
-extern "C" int pc_adam_segments(double* params, const float* grads, double* m, double* v,
-                                int32_t n_seg, const int64_t* seg_off, const double* seg_lr,
-                                const int32_t* seg_step, const double* seg_floor,
-                                pc_stream_t stream) {
+extern "C" int pc_check_finite(const float* x, int32_t n_seg, const int64_t* seg_off,
+                               int32_t* flags, pc_stream_t stream) {
+    return check_finite_impl(x, n_seg, seg_off, flags, stream);
+}
+
+extern "C" int pc_check_finite_f64(const double* x, int32_t n_seg, const int64_t* seg_off,
+                                   int32_t* flags, pc_stream_t stream) {
+    return check_finite_impl(x, n_seg, seg_off, flags, stream);
+}
+
+template <typename GT>
+static int adam_impl(double* params, const GT* grads, double* m, double* v, int32_t n_seg,
+                     const int64_t* seg_off, const double* seg_lr, const int32_t* seg_step,
+                     const double* seg_floor, pc_stream_t stream) {
     SegTable t;
     if (!seg_table(n_seg, seg_off, t) || !seg_lr || !seg_step) return PC_ERR_ARGUMENT;
     if (t.off[n_seg] > t.off[0] && (!params || !grads || !m || !v)) return PC_ERR_ARGUMENT;
@@ -365,8 +379,22 @@ extern "C" int pc_adam_segments(double* params, const float* grads, double* m, d
         t.bc2[s] = 1.0 - pow(kBeta2, (double)seg_step[s]);
         t.floor_[s] = seg_floor ? seg_floor[s] : -INFINITY;
     }
-    k_adam<<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(params, grads, m, v, t);
+    k_adam<GT><<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(params, grads, m, v, t);
     return last_status();
+}
+
+extern "C" int pc_adam_segments(double* params, const float* grads, double* m, double* v,
+                                int32_t n_seg, const int64_t* seg_off, const double* seg_lr,
+                                const int32_t* seg_step, const double* seg_floor,
+                                pc_stream_t stream) {
+    return adam_impl(params, grads, m, v, n_seg, seg_off, seg_lr, seg_step, seg_floor, stream);
+}
+
+extern "C" int pc_adam_segments_f64(double* params, const double* grads, double* m, double* v,
+                                    int32_t n_seg, const int64_t* seg_off, const double* seg_lr,
+                                    const int32_t* seg_step, const double* seg_floor,
+                                    pc_stream_t stream) {
+    return adam_impl(params, grads, m, v, n_seg, seg_off, seg_lr, seg_step, seg_floor, stream);
 }
 
 // Guarded update (no host round trip between the gradient and the step):
@@ -397,19 +425,21 @@ __global__ void __launch_bounds__(256) k_update_guarded(double* __restrict__ p,
     // per thread cost 2.5x the whole update)
     __shared__ double sh[3];
     if (threadIdx.x == 0) {
-        int bad = 0x7fffffff;
-        for (int k = 0; k < t.n; ++k)
-            if (flags[k]) bad = min(bad, t.group[k]);
-        const bool go = isfinite(*loss) && *coinc == 0x7fffffffffffffffLL && t.group[s] < bad;
+        int bad = t.n;                          // first segment with a non-finite gradient
+        for (int k = t.n - 1; k >= 0; --k)
+            if (flags[k]) bad = k;
+        const bool go = isfinite(*loss) && *coinc == 0x7fffffffffffffffLL && s < bad;
         const double step = hyper[2 * s + 1];
-        sh[0] = go ? 1.0 : 0.0;
+        // floors only when every segment stepped: the reference raises out
+        // of ParamGroup.step before _clamp_floors (reconstruction.py:320-328)
+        sh[0] = go ? (bad == t.n ? 2.0 : 1.0) : 0.0;
         sh[1] = 1.0 - pow(kBeta1, step);
         sh[2] = 1.0 - pow(kBeta2, step);
     }
     __syncthreads();
     if (sh[0] == 0.0) return;
     const int64_t lo = t.off[s], hi = t.off[s + 1];
-    const double lr = hyper[2 * s], fl = t.floor_[s];
+    const double lr = hyper[2 * s], fl = sh[0] == 2.0 ? t.floor_[s] : -INFINITY;
     const double bc1 = sh[1], bc2 = sh[2];
     for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -455,9 +485,9 @@ extern "C" int pc_update_guarded(double* params, const float* grads, double* m, 
     return last_status();
 }
 
-extern "C" int pc_sgd_segments(double* params, const float* grads, int32_t n_seg,
-                               const int64_t* seg_off, const double* seg_lr,
-                               const double* seg_floor, pc_stream_t stream) {
+template <typename GT>
+static int sgd_impl(double* params, const GT* grads, int32_t n_seg, const int64_t* seg_off,
+                    const double* seg_lr, const double* seg_floor, pc_stream_t stream) {
     SegTable t;
     if (!seg_table(n_seg, seg_off, t) || !seg_lr) return PC_ERR_ARGUMENT;
     if (t.off[n_seg] > t.off[0] && (!params || !grads)) return PC_ERR_ARGUMENT;
@@ -466,8 +496,20 @@ extern "C" int pc_sgd_segments(double* params, const float* grads, int32_t n_seg
         t.floor_[s] = seg_floor ? seg_floor[s] : -INFINITY;
         t.bc1[s] = t.bc2[s] = 1.0;
     }
-    k_sgd<<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(params, grads, t);
+    k_sgd<GT><<<dim3(seg_blocks(t), n_seg), 256, 0, as_stream(stream)>>>(params, grads, t);
     return last_status();
+}
+
+extern "C" int pc_sgd_segments(double* params, const float* grads, int32_t n_seg,
+                               const int64_t* seg_off, const double* seg_lr,
+                               const double* seg_floor, pc_stream_t stream) {
+    return sgd_impl(params, grads, n_seg, seg_off, seg_lr, seg_floor, stream);
+}
+
+extern "C" int pc_sgd_segments_f64(double* params, const double* grads, int32_t n_seg,
+                                   const int64_t* seg_off, const double* seg_lr,
+                                   const double* seg_floor, pc_stream_t stream) {
+    return sgd_impl(params, grads, n_seg, seg_off, seg_lr, seg_floor, stream);
 }
 
 extern "C" size_t pc_compact_workspace_bytes(int64_t n_balls) {

@@ -235,6 +235,7 @@ struct FwdArgs {
     float inv_v_f, t0_f, inv_dt_f, sa_f, vt0_f, vdt_f;
     double vdt_d, vt0_d;
     int part_margin;     // > 0: partial rows written over the active range +- margin only
+    long long fo, so, mt; // coincidence word: frame offset, sensor offset, total sensors
 };
 
 // s = sqrt(log2 e / 2) / a0 by the approximate division (2 ulp: x and the
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(FWD_WARPS * 32) k_forward(FwdArgs a) {
                            s1, q);
 #endif
                 if (q.R < kCoincidenceEps) {
-                    atomicMin(a.coinc, (long long)(b0 + i) * a.M + m);
+                    atomicMin(a.coinc, ((a.fo + f) * a.B + b0 + i) * a.mt + a.so + m);
                     pass = false;
                 } else if (q.jh <= q.jl) {
                     pass = false;
@@ -900,6 +901,7 @@ struct AdjArgs {
     int F, M;
     ArrayConsts ac;
     int msplit;     // SPLIT: first sensor of the second half (multiple of 32)
+    long long fo, so, mt; // coincidence word: frame offset, sensor offset, total sensors
 };
 
 // Residual samples j .. j+3 (one 16-byte load when rows are 16-byte aligned).
@@ -999,7 +1001,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             PairSetup q;
             pair_setup(dx, dy, dz, av, s, a.ac, 0, T, q);
             if (q.R < kCoincidenceEps) {
-                atomicMin(a.coinc, (long long)b * a.M + m);
+                atomicMin(a.coinc, ((a.fo + f) * a.B + b) * a.mt + a.so + m);
             } else if (q.jh > q.jl) {
                 win = q.jl | (q.near ? 1 << 30 : 0);
                 wh = q.jh;
@@ -1344,7 +1346,7 @@ __global__ void __launch_bounds__(TW * 32) k_adjoint_tma(AdjArgs a) {
             PairSetup q;
             pair_setup(dx, dy, dz, av, s, a.ac, 0, T, q);
             if (q.R < kCoincidenceEps) {
-                atomicMin(a.coinc, (long long)b * a.M + m);
+                atomicMin(a.coinc, ((a.fo + f) * a.B + b) * a.mt + a.so + m);
             } else if (q.jh > q.jl) {
                 win = q.jl | (q.near ? 1 << 30 : 0);
                 wh = q.jh;
@@ -1528,11 +1530,29 @@ static bool fwd_pm() {
     return v != 0;
 }
 
+// The register-run forward (fwd_run.cu) is the default; PC_FWD_LEGACY=1
+// selects the shared-memory-trace kernel above (kept for A/B measurements).
+static bool fwd_legacy(const pc_array_t* array) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PC_FWD_LEGACY");
+        v = e ? atoi(e) != 0 : 0;
+    }
+    return v != 0 || !fwd_run_supported(array);
+}
+
 extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array_t* array,
                                int32_t* plan) {
     if (!array || !plan || n_balls < 0 || n_frames < 1 || array->n_sensors < 1 ||
         array->n_samples < 1)
         return PC_ERR_ARGUMENT;
+    if (!fwd_legacy(array)) {
+        plan[0] = fwd_run_samples_per_run();
+        plan[1] = 1;
+        plan[2] = 1;
+        plan[3] = 2;   // forward + loss reduce
+        return PC_OK;
+    }
     FwdPlan p = fwd_plan(n_balls > 0 ? n_balls : 1, n_frames, array->n_sensors,
                          array->n_samples);
     plan[0] = p.Tseg;
@@ -1545,6 +1565,7 @@ extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array
 extern "C" size_t pc_forward_workspace_bytes(int64_t n_balls, int32_t n_frames,
                                              const pc_array_t* array) {
     if (!array || n_balls < 0 || n_frames < 1) return 0;
+    if (!fwd_legacy(array)) return fwd_run_workspace_bytes(n_frames, array);
     FwdPlan p = fwd_plan(n_balls > 0 ? n_balls : 1, n_frames, array->n_sensors,
                          array->n_samples);
     return p.prep_bytes + p.partial_bytes + p.loss_bytes + 256;
@@ -1562,6 +1583,26 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
     const int M = array->n_sensors, T = array->n_samples, F = n_frames;
     cudaStream_t st = as_stream(stream);
     if (n_balls > 0 && (!mu_t || !a0_t || !p0_t)) return PC_ERR_ARGUMENT;
+    if (!fwd_legacy(array)) {
+        const bool want_loss = observed && loss_per_frame;
+        if (want_loss && (!workspace || workspace_bytes < fwd_run_workspace_bytes(F, array)))
+            return PC_ERR_ARGUMENT;
+        double* lpart = reinterpret_cast<double*>(workspace);
+        if (n_balls > 0) {
+            const int rc = fwd_run_launch(mu_t, a0_t, p0_t, n_balls, F, array, ac, observed, out,
+                                          want_loss ? lpart : nullptr, coincident, st);
+            if (rc != PC_OK) return rc;
+        } else {
+            if (cudaMemsetAsync(out, 0, (size_t)F * M * T * sizeof(float), st) != cudaSuccess)
+                return PC_ERR_CUDA;
+            if (observed)
+                k_forward_finish<<<dim3(M, F), 256, 0, st>>>(
+                    out, observed, out, want_loss ? lpart : nullptr, 1, F, M, T,
+                    finish_vec(out, observed, out, T));
+        }
+        if (want_loss) k_loss_reduce<<<F, 256, 0, st>>>(lpart, M, loss_per_frame);
+        return last_status();
+    }
     FwdPlan p = fwd_plan(n_balls > 0 ? n_balls : 1, F, M, T);
     const size_t need = p.partial_bytes + p.loss_bytes + p.prep_bytes;
     if (!workspace || workspace_bytes < need) return PC_ERR_ARGUMENT;
@@ -1595,6 +1636,9 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
         a.out = p.nchunk > 1 ? partial : out;
         a.loss = (want_loss && p.nchunk == 1) ? lpart : nullptr;
         a.coinc = reinterpret_cast<long long*>(coincident);
+        a.fo = array->frame_offset;
+        a.so = array->sensor_offset;
+        a.mt = array->n_sensors_total > 0 ? array->n_sensors_total : M;
         a.B = n_balls;
         a.F = F;
         a.M = M;
@@ -1711,6 +1755,9 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     a.resid = residual;
     a.G = G;
     a.coinc = reinterpret_cast<long long*>(coincident);
+    a.fo = array->frame_offset;
+    a.so = array->sensor_offset;
+    a.mt = array->n_sensors_total > 0 ? array->n_sensors_total : array->n_sensors;
     a.B = n_balls;
     a.F = n_frames;
     a.M = array->n_sensors;
@@ -1754,5 +1801,53 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     } else {
         k_adjoint<false, false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
     }
+    return last_status();
+}
+
+// ---------------------------------------------------------------- formula anchors
+//
+// radiator.py:36-55 pressure_kernel and :58-83 pressure_kernel_grad,
+// elementwise in fp64 over already-broadcast inputs (the reference's
+// closed form, term for term).
+__global__ void __launch_bounds__(256) k_pressure(const double* __restrict__ R,
+                                                  const double* __restrict__ t,
+                                                  const double* __restrict__ p0,
+                                                  const double* __restrict__ a0, int64_t n,
+                                                  double v, double* __restrict__ out,
+                                                  double* __restrict__ d_p0,
+                                                  double* __restrict__ d_a0,
+                                                  double* __restrict__ d_R) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double r = R[i], tt = t[i], p = p0[i], a = a0[i];
+        const double um = r - v * tt, up = r + v * tt;
+        if (out) {
+            const double inv2a2 = 1.0 / (2.0 * (a * a));
+            out[i] = (p / (2.0 * r)) * (um * exp(-um * um * inv2a2) + up * exp(-up * up * inv2a2));
+        }
+        if (d_p0) {
+            const double inv_a2 = 1.0 / (a * a);
+            const double gm = exp(-0.5 * um * um * inv_a2);
+            const double gp = exp(-0.5 * up * up * inv_a2);
+            const double s = um * gm + up * gp;
+            d_p0[i] = s / (2.0 * r);
+            d_a0[i] = (p / (2.0 * r)) * (um * um * um * gm + up * up * up * gp) * inv_a2 / a;
+            const double ds = gm * (1.0 - um * um * inv_a2) + gp * (1.0 - up * up * inv_a2);
+            d_R[i] = -(p * s) / (2.0 * r * r) + (p / (2.0 * r)) * ds;
+        }
+    }
+}
+
+extern "C" int pc_pressure_kernel(const double* R, const double* t, const double* p0,
+                                  const double* a0, int64_t n, double sound_speed, double* out,
+                                  double* d_p0, double* d_a0, double* d_R, pc_stream_t stream) {
+    if (n < 0 || !(sound_speed > 0)) return PC_ERR_ARGUMENT;
+    if (n == 0) return PC_OK;
+    if (!R || !t || !p0 || !a0 || (!out && !d_p0)) return PC_ERR_ARGUMENT;
+    if (d_p0 && (!d_a0 || !d_R)) return PC_ERR_ARGUMENT;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    k_pressure<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(R, t, p0, a0, n, sound_speed, out,
+                                                                d_p0, d_a0, d_R);
     return last_status();
 }

@@ -15,6 +15,7 @@ bit-exactly, as deformation.py:119-120 requires.
 from __future__ import annotations
 
 import ctypes
+import math
 
 import numpy as np
 import torch
@@ -82,7 +83,7 @@ def deform_states_device(dcloud: DeviceCloud, t_frames, coord_mode,
         p0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
     if H is None:
         H = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
-    floor = -1.0 if a0_floor is None else float(a0_floor)
+    floor = math.nan if a0_floor is None else float(a0_floor)
     _lib.check(lib.pc_deform_states(
         ctypes.byref(dcloud.struct), _lib.ptr(t_frames), F,
         _lib.PC_COORD[coord_mode], floor, _lib.ptr(mu_t), _lib.ptr(a0_t),
@@ -95,7 +96,7 @@ def deform_backward_device(dcloud: DeviceCloud, t_frames, coord_mode,
     """pc_deform_backward: `grads` maps p0/a0/mu/theta/sigma/omega to f32
     device tensors shaped like the cloud (overwritten)."""
     lib = _lib.load_library()
-    floor = -1.0 if a0_floor is None else float(a0_floor)
+    floor = math.nan if a0_floor is None else float(a0_floor)
     gs = _lib.PcCloudGrads(
         _lib.ptr(grads["p0"]), _lib.ptr(grads["a0"]), _lib.ptr(grads["mu"]),
         _lib.ptr(grads.get("theta")), _lib.ptr(grads.get("sigma")),
@@ -124,9 +125,19 @@ def cloud_states_at(cloud, t: float, coord_mode: str = "multiplicative",
         st = (z, z.clone(), torch.zeros((0, 3), dtype=torch.float64,
                                          device=_device()))
     else:
-        mu_t, a0_t, p0_t, _ = deform_states_device(dc, tf, coord_mode,
-                                                   a0_floor)
-        st = (a0_t[0].double(), p0_t[0].double(), mu_t[0])
+        # float64 a0_t / p0_t like the reference's CloudState (the engine's
+        # radiator path keeps its own float32 copies)
+        lib = _lib.load_library()
+        f64 = dict(dtype=torch.float64, device=_device())
+        mu_t = torch.empty((1, dc.B, 3), **f64)
+        a0_t = torch.empty((1, dc.B), **f64)
+        p0_t = torch.empty((1, dc.B), **f64)
+        floor = math.nan if a0_floor is None else float(a0_floor)
+        _lib.check(lib.pc_deform_states_f64(
+            ctypes.byref(dc.struct), _lib.ptr(tf), 1,
+            _lib.PC_COORD[coord_mode], floor, _lib.ptr(mu_t), _lib.ptr(a0_t),
+            _lib.ptr(p0_t), _lib.stream()), "pc_deform_states_f64")
+        st = (a0_t[0], p0_t[0], mu_t[0])
     if not torch_io:
         st = tuple(x.cpu().numpy() for x in st)
     return CloudState(*st)
@@ -147,7 +158,7 @@ def cloud_state_grads(cloud, t: float, coord_mode: str = "multiplicative",
     d_th = torch.zeros((B, 5, N), **f64) if gauss else torch.zeros((B, 0), **f64)
     d_sg = torch.zeros((B, 5, N), **f64) if gauss else torch.zeros((B, 0), **f64)
     if B:
-        floor = -1.0 if a0_floor is None else float(a0_floor)
+        floor = math.nan if a0_floor is None else float(a0_floor)
         _lib.check(lib.pc_deform_jacobian(
             ctypes.byref(dc.struct), float(t), _lib.PC_COORD[coord_mode],
             floor, _lib.ptr(d_base), _lib.ptr(d_om),
@@ -159,3 +170,116 @@ def cloud_state_grads(cloud, t: float, coord_mode: str = "multiplicative",
         out = [x.cpu().numpy() for x in out]
     shared = (not gauss) or not dc.per_channel
     return CloudStateGrad(*out, omega_rows(coord_mode), shared)
+
+
+# ---------------------------------------------------------------- single ball
+
+def eval_basis(t, theta, sigma):
+    """deformation.py:57-70: exp(-(t - theta)^2 / (2 sigma^2)), broadcasting
+    (pc_eval_basis, fp64 on the device)."""
+    theta = np.asarray(theta, dtype=np.float64)
+    sigma = np.asarray(sigma, dtype=np.float64)
+    if np.any(sigma <= 0):
+        raise ValueError("basis width sigma must be > 0")
+    lib = _lib.load_library()
+    arrs = np.broadcast_arrays(np.asarray(t, dtype=np.float64), theta, sigma)
+    shape = arrs[0].shape
+    dev = [torch.as_tensor(np.ascontiguousarray(x).reshape(-1),
+                           device=_device()) for x in arrs]
+    out = torch.empty(dev[0].numel(), dtype=torch.float64, device=_device())
+    _lib.check(lib.pc_eval_basis(*[_lib.ptr(x) for x in dev], out.numel(),
+                                 _lib.ptr(out), _lib.stream()),
+               "pc_eval_basis")
+    res = out.cpu().numpy().reshape(shape)
+    return float(res) if res.ndim == 0 else res
+
+
+def eval_H(t: float, omega, theta, sigma) -> float:
+    """deformation.py:73-84: weighted Gaussian-basis sum; zero weights give
+    exactly 0 (pc_eval_h, fp64 on the device)."""
+    omega = np.asarray(omega, dtype=np.float64)
+    theta = np.asarray(theta, dtype=np.float64)
+    sigma = np.asarray(sigma, dtype=np.float64)
+    if not (omega.shape == theta.shape == sigma.shape) or omega.ndim != 1:
+        raise ValueError(
+            f"omega, theta, sigma must be 1-d with equal lengths, got "
+            f"{omega.shape}, {theta.shape}, {sigma.shape}")
+    if not np.any(omega):
+        return 0.0
+    if np.any(sigma <= 0):
+        raise ValueError("basis width sigma must be > 0")
+    lib = _lib.load_library()
+    dev = [torch.as_tensor(x, device=_device()) for x in (omega, theta, sigma)]
+    out = torch.empty(1, dtype=torch.float64, device=_device())
+    _lib.check(lib.pc_eval_h(float(t), *[_lib.ptr(x) for x in dev],
+                             len(omega), _lib.ptr(out), _lib.stream()),
+               "pc_eval_h")
+    return float(out.item())
+
+
+def _one_ball_cloud(ball, deform):
+    """A one-ball Gaussian-basis DeviceCloud (shared (1,N) or per-channel
+    (1,5,N) theta/sigma) for the single-ball drop-ins."""
+    f = lambda x: torch.as_tensor(np.asarray(x, dtype=np.float64)[None],  # noqa: E731
+                                  device=_device()).contiguous()
+    return DeviceCloud(f(ball.p0), f(ball.a0), f(ball.mu), f(deform.theta),
+                       f(deform.sigma), f(deform.omega), "gauss")
+
+
+def ball_state_at(ball, deform, t: float, coord_mode: str = "multiplicative",
+                  a0_floor: float | None = None):
+    """deformation.py:102-130: one ball at normalized time t (the batched
+    kernel on a one-ball cloud; zero weights reproduce the baseline
+    bit-exactly)."""
+    from .core import BallStateAtT
+    _check_mode(coord_mode)
+    lib = _lib.load_library()
+    dc = _one_ball_cloud(ball, deform)
+    f64 = dict(dtype=torch.float64, device=_device())
+    tf = torch.tensor([float(t)], **f64)
+    mu_t = torch.empty((1, 1, 3), **f64)
+    a0_t = torch.empty((1, 1), **f64)
+    p0_t = torch.empty((1, 1), **f64)
+    floor = math.nan if a0_floor is None else float(a0_floor)
+    _lib.check(lib.pc_deform_states_f64(
+        ctypes.byref(dc.struct), _lib.ptr(tf), 1, _lib.PC_COORD[coord_mode],
+        floor, _lib.ptr(mu_t), _lib.ptr(a0_t), _lib.ptr(p0_t), _lib.stream()),
+        "pc_deform_states_f64")
+    return BallStateAtT(float(a0_t.item()), float(p0_t.item()),
+                        mu_t[0, 0].cpu().numpy())
+
+
+class BallStateGrad:
+    """deformation.py:133-150: partials of one ball's state (rows in state
+    order a0_t, p0_t, mu_x, mu_y, mu_z)."""
+
+    def __init__(self, d_base, d_omega, d_theta, d_sigma, omega_row,
+                 shared_basis):
+        self.d_base = d_base
+        self.d_omega = d_omega
+        self.d_theta = d_theta
+        self.d_sigma = d_sigma
+        self.omega_row = omega_row
+        self.shared_basis = shared_basis
+
+
+def ball_state_grad(ball, deform, t: float,
+                    coord_mode: str = "multiplicative") -> BallStateGrad:
+    """deformation.py:153-181: exact partials of ball_state_at (no floor;
+    pc_deform_jacobian on a one-ball cloud)."""
+    _check_mode(coord_mode)
+    lib = _lib.load_library()
+    dc = _one_ball_cloud(ball, deform)
+    N = dc.N
+    f64 = dict(dtype=torch.float64, device=_device())
+    d_base = torch.zeros((1, 5), **f64)
+    d_om = torch.zeros((1, 5, N), **f64)
+    d_th = torch.zeros((1, 5, N), **f64)
+    d_sg = torch.zeros((1, 5, N), **f64)
+    _lib.check(lib.pc_deform_jacobian(
+        ctypes.byref(dc.struct), float(t), _lib.PC_COORD[coord_mode],
+        math.nan, _lib.ptr(d_base), _lib.ptr(d_om), _lib.ptr(d_th),
+        _lib.ptr(d_sg), _lib.stream()), "pc_deform_jacobian")
+    return BallStateGrad(d_base[0].cpu().numpy(), d_om[0].cpu().numpy(),
+                         d_th[0].cpu().numpy(), d_sg[0].cpu().numpy(),
+                         omega_rows(coord_mode), bool(deform.theta.ndim == 1))

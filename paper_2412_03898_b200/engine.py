@@ -140,8 +140,10 @@ class IterationEngine:
                   if self.shard == "sensors" else (0, array.n_sensors))
         self.sensors = (int(lo), int(hi))
         pos = np.asarray(array.positions)[lo:hi]
+        self.positions_all = np.asarray(array.positions, dtype=np.float64)
         self.darr = DeviceArray(array, config.support_sigmas,
-                                config.exact_forward, positions=pos)
+                                config.exact_forward, positions=pos,
+                                sensor_offset=int(lo))
         # observed: (F_all, M_local, T) float32 on the device
         obs = observed
         if not isinstance(obs, torch.Tensor):
@@ -264,6 +266,13 @@ class IterationEngine:
             return frame_shard(frames, self.rank, self.world)
         return np.asarray(frames, dtype=np.int64)
 
+    def _frame_offset(self, frames: np.ndarray) -> int:
+        """Position of this rank's first frame in the iteration's frame
+        list (the coincidence word's frame index is global)."""
+        if self.shard == "frames":
+            return shard_range(len(frames), self.rank, self.world)[0]
+        return 0
+
     # ------------------------------------------------------------ compute
     def _launch_compute(self, obs, host_src=None):
         """deform -> forward+loss -> adjoint -> deformation backward.
@@ -328,6 +337,8 @@ class IterationEngine:
     def compute_grads(self, frames: np.ndarray) -> None:
         """Launch (asynchronously) the gradient of the selected frames."""
         local = self._local_frames(np.asarray(frames))
+        fo = self._frame_offset(np.asarray(frames))
+        self.darr.struct.frame_offset = int(fo)
         F = len(local)
         if F == 0:
             self.Gf.zero_()
@@ -353,7 +364,7 @@ class IterationEngine:
             else:
                 idx = torch.as_tensor(local, device=self.device)
                 torch.index_select(self.observed, 0, idx, out=self.obs_stage)
-        key = (tuple(int(k) for k in local),
+        key = (tuple(int(k) for k in local), int(fo),
                None if host is None else host.data_ptr())
         if self.use_graph and self._graph is not None \
                 and self._graph_frames == key:
@@ -576,23 +587,44 @@ class IterationEngine:
         self._guarded_update(lrs)
         loss, flags, coinc = self._status()
         if coinc != _lib.INT64_MAX:
-            b, m = divmod(coinc, self.darr.M)
-            raise_if_coincident(int(self.order[b]) * self.darr.M + m,
-                                self.mu_t[0][torch.as_tensor(self.inverse, device=self.device)],
-                                self.darr.positions)
+            self._raise_coincident(coinc, frames)
         if not math.isfinite(loss):
             raise RuntimeError(f"non-finite loss at iteration {iteration}")
-        bad = len(GROUP_ORDER)
+        # adam_step raises per ARRAY before touching it (reconstruction.py:
+        # 60-61, 88-93): the segments before the first non-finite one were
+        # stepped (pc_update_guarded did the same on the device)
+        segs = self.layout.segments
+        bad = len(segs)
         if flags.any():
-            bad = min(GROUP_ORDER.index(self.layout.segments[i].group)
-                      for i in np.nonzero(flags)[0])
-        for sg in self.layout.segments:        # the segments stepped
-            if GROUP_ORDER.index(sg.group) < bad:
-                self.step_count[sg.name] += 1
-        if bad < len(GROUP_ORDER):
+            bad = int(np.nonzero(flags)[0][0])
+        for sg in segs[:bad]:
+            self.step_count[sg.name] += 1
+        if bad < len(segs):
             raise ValueError(
-                f"non-finite gradient in parameter group '{GROUP_ORDER[bad]}'")
+                f"non-finite gradient in parameter group '{segs[bad].group}'")
         return loss
+
+    def _raise_coincident(self, word: int, frames) -> None:
+        """reconstruction.py:303-311 -> radiator.py:186-192: the first frame
+        of the iteration (in frame-list order) holding a coincident pair
+        raises, naming the closest (ball, sensor) pair of THAT frame over the
+        whole array.  The word ((f B + b) M_total + m, MIN-reduced over
+        ranks) names the frame; its states are recomputed here (parameters
+        are replicated), so every rank raises the same message."""
+        frames = np.asarray(frames, dtype=np.int64)
+        fpos = int(word) // (self.B * self.darr.n_sensors_total)
+        k = int(frames[min(fpos, len(frames) - 1)])
+        dev, B = self.device, self.B
+        t = torch.tensor([self.frame_times_all[k]], dtype=torch.float64,
+                         device=dev)
+        mu1 = torch.empty((1, B, 3), dtype=torch.float64, device=dev)
+        a1 = torch.empty((1, B), dtype=torch.float32, device=dev)
+        p1 = torch.empty((1, B), dtype=torch.float32, device=dev)
+        deform_states_device(self.dcloud, t, self.cfg.coord_mode,
+                             self.cfg.a0_floor, mu1, a1, p1, None)
+        inv = torch.as_tensor(self.inverse, device=dev)
+        raise_if_coincident(word, mu1[0].index_select(0, inv),
+                            self.positions_all)
 
     # ------------------------------------------------------------ densify
     def p0_grad_threshold(self, q: float = 90.0) -> float:

@@ -15,6 +15,7 @@ over-frames layer the fused engine uses.
 from __future__ import annotations
 
 import ctypes
+import math
 
 import numpy as np
 import torch
@@ -63,7 +64,7 @@ class DeviceArray:
     """A SensorArray resident on the device plus its pc_array_t."""
 
     def __init__(self, array, support_sigmas=DEFAULT_SUPPORT_SIGMAS,
-                 exact=False, positions=None):
+                 exact=False, positions=None, sensor_offset=0):
         _lib.load_library()
         self.array = array
         self.positions = to_device(
@@ -76,13 +77,16 @@ class DeviceArray:
         self.dt = 1.0 / float(array.sample_rate)
         self.support = float(support_sigmas)
         self.exact = bool(exact)
+        n_total = int(np.shape(array.positions)[0])
         self.order = torch.as_tensor(
             sensor_cluster_order(self.positions.double().cpu().numpy()),
             dtype=torch.int32, device=self.positions.device)
         self.struct = _lib.PcArray(
             self.positions.data_ptr(), self.M, self.T, self.v, self.t0,
-            self.dt, self.support, int(self.exact), 0,
-            self.order.data_ptr())
+            self.dt, self.support, int(self.exact), int(sensor_offset),
+            self.order.data_ptr(), n_total, 0)
+        self.sensor_offset = int(sensor_offset)
+        self.n_sensors_total = n_total
 
     def plan(self, n_balls: int, n_frames: int) -> dict:
         """pc_forward_plan: time segment, segments, ball chunks, launches."""
@@ -170,19 +174,33 @@ def state_grads_device(darr: DeviceArray, mu_t, a0_t, p0_t, residual,
     return G, coincident
 
 
+def coincident_pair(mu, positions, chunk: int = 1 << 16):
+    """radiator.py:186-192 _raise_coincident's pair: the first (ball, sensor)
+    of the smallest distance |mu_b - s_m| in C order (numpy argmin), and
+    that distance.  Computed on the device in ball chunks (fp64)."""
+    mu = to_device(mu, torch.float64).reshape(-1, 3)
+    pos = to_device(positions, torch.float64).reshape(-1, 3)
+    best, bb, mm = math.inf, 0, 0
+    for b0 in range(0, mu.shape[0], chunk):
+        d = torch.sqrt(((mu[b0:b0 + chunk, None, :] - pos[None, :, :]) ** 2)
+                       .sum(dim=2))
+        k = int(torch.argmin(d).item())
+        b, m = divmod(k, pos.shape[0])
+        v = float(d[b, m].item())
+        if v < best:
+            best, bb, mm = v, b0 + b, m
+    return bb, mm, best
+
+
 def raise_if_coincident(coincident, mu_t, positions):
-    """radiator.py:186-192: ValueError naming the coincident (ball, sensor)."""
+    """radiator.py:186-192: if the device coincidence word is set, raise the
+    reference's ValueError naming the closest (ball, sensor) pair of the
+    frame (mu_t: that frame's centres, positions: the whole array)."""
     c = int(coincident.item()) if isinstance(coincident, torch.Tensor) \
         else int(coincident)
     if c == _lib.INT64_MAX:
         return
-    M = int(positions.shape[0])
-    b, m = divmod(c, M)
-    mu = mu_t.reshape(-1, 3)[b].double().cpu().numpy() \
-        if isinstance(mu_t, torch.Tensor) else np.asarray(mu_t)[b]
-    pos = positions[m].double().cpu().numpy() \
-        if isinstance(positions, torch.Tensor) else np.asarray(positions)[m]
-    d = float(np.linalg.norm(mu - pos))
+    b, m, d = coincident_pair(mu_t, positions)
     raise ValueError(f"ball {b} coincides with sensor {m} "
                      f"(distance {d:.3g} mm)")
 
@@ -208,6 +226,54 @@ def compute_time_window(array, roi, margin_a0: float):
 
 
 # ---------------------------------------------------------------- drop-ins
+
+def _eval_pressure(R, t, p0, a0, v, grad):
+    """Broadcast on the host (numpy rules), evaluate on the device."""
+    lib = _lib.load_library()
+    arrs = np.broadcast_arrays(*[np.asarray(x, dtype=np.float64)
+                                 for x in (R, t, p0, a0)])
+    shape = arrs[0].shape
+    dev = [torch.as_tensor(np.ascontiguousarray(x).reshape(-1),
+                           device=_device()) for x in arrs]
+    n = dev[0].numel()
+    outs = [torch.empty(n, dtype=torch.float64, device=_device())
+            for _ in range(3 if grad else 1)]
+    if grad:
+        args = (None, _lib.ptr(outs[0]), _lib.ptr(outs[1]), _lib.ptr(outs[2]))
+    else:
+        args = (_lib.ptr(outs[0]), None, None, None)
+    _lib.check(lib.pc_pressure_kernel(*[_lib.ptr(x) for x in dev], n,
+                                      float(v), *args, _lib.stream()),
+               "pc_pressure_kernel")
+    res = [o.cpu().numpy().reshape(shape) for o in outs]
+    if len(shape) == 0:
+        res = [float(x) for x in res]
+    return res
+
+
+def pressure_kernel(R, t, p0, a0, v):
+    """Pressure radiated by one Gaussian ball, broadcasting over inputs
+    (radiator.py:36-55; evaluated on the device in fp64)."""
+    R = np.asarray(R, dtype=np.float64)
+    if np.any(R <= 0):
+        raise ValueError("source-sensor distance R must be > 0 "
+                         "(sensor coincides with the ball center)")
+    if not (np.all(np.asarray(a0) > 0) and v > 0):
+        raise ValueError("a0 and v must be > 0")
+    return _eval_pressure(R, t, p0, a0, v, grad=False)[0]
+
+
+def pressure_kernel_grad(R, t, p0, a0, v):
+    """Partials of pressure_kernel w.r.t. (p0, a0, R), broadcasting
+    (radiator.py:58-83; evaluated on the device in fp64)."""
+    R = np.asarray(R, dtype=np.float64)
+    if np.any(R <= 0):
+        raise ValueError("source-sensor distance R must be > 0")
+    if not (np.all(np.asarray(a0) > 0) and v > 0):
+        raise ValueError("a0 and v must be > 0")
+    d_p0, d_a0, d_R = _eval_pressure(R, t, p0, a0, v, grad=True)
+    return d_p0, d_a0, d_R
+
 
 def _as_cloud_state(states):
     """radiator.py:177-183."""

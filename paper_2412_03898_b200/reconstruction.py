@@ -46,12 +46,13 @@ def l2_loss(predicted, observed) -> float:
     return float(out.item())
 
 
-def _finite_or_raise(g32: torch.Tensor, group: str) -> None:
+def _finite_or_raise(g: torch.Tensor, group: str) -> None:
+    """reconstruction.py:60-61 on the caller's float64 gradient."""
     lib = _lib.load_library()
-    flags = torch.zeros(1, dtype=torch.int32, device=g32.device)
-    _lib.check(lib.pc_check_finite(
-        _lib.ptr(g32), 1, _lib.i64_array([0, g32.numel()]), _lib.ptr(flags),
-        _lib.stream()), "pc_check_finite")
+    flags = torch.zeros(1, dtype=torch.int32, device=g.device)
+    _lib.check(lib.pc_check_finite_f64(
+        _lib.ptr(g), 1, _lib.i64_array([0, g.numel()]), _lib.ptr(flags),
+        _lib.stream()), "pc_check_finite_f64")
     if int(flags.item()):
         raise ValueError(f"non-finite gradient in parameter group '{group}'")
 
@@ -65,9 +66,10 @@ def _inplace(param, dev_value: torch.Tensor) -> None:
 
 def adam_step(param, grad, state: AdamState, lr: float,
               group: str = "") -> None:
-    """One in-place Adam update (beta1 0.9, beta2 0.999, eps 1e-8)."""
+    """One in-place Adam update (beta1 0.9, beta2 0.999, eps 1e-8), in
+    float64 like reconstruction.py:57-69 (pc_adam_segments_f64)."""
     lib = _lib.load_library()
-    g = to_device(grad, torch.float32).reshape(-1)
+    g = to_device(grad, torch.float64).reshape(-1)
     if g.numel() != int(np.prod(np.shape(param))):
         raise ValueError("grad and param sizes differ")
     _finite_or_raise(g, group)
@@ -76,26 +78,27 @@ def adam_step(param, grad, state: AdamState, lr: float,
     v = to_device(state.v, torch.float64).reshape(-1).clone()
     state.t += 1
     if p.numel():
-        _lib.check(lib.pc_adam_segments(
+        _lib.check(lib.pc_adam_segments_f64(
             _lib.ptr(p), _lib.ptr(g), _lib.ptr(m), _lib.ptr(v), 1,
             _lib.i64_array([0, p.numel()]), _lib.f64_array([lr]),
             _lib.i32_array([state.t]), _lib.f64_array([-math.inf]),
-            _lib.stream()), "pc_adam_segments")
+            _lib.stream()), "pc_adam_segments_f64")
     _inplace(param, p)
     _inplace(state.m, m)
     _inplace(state.v, v)
 
 
 def sgd_step(param, grad, lr: float, group: str = "") -> None:
+    """reconstruction.py:72-76 in float64 (pc_sgd_segments_f64)."""
     lib = _lib.load_library()
-    g = to_device(grad, torch.float32).reshape(-1)
+    g = to_device(grad, torch.float64).reshape(-1)
     _finite_or_raise(g, group)
     p = to_device(param, torch.float64).reshape(-1).clone()
     if p.numel():
-        _lib.check(lib.pc_sgd_segments(
+        _lib.check(lib.pc_sgd_segments_f64(
             _lib.ptr(p), _lib.ptr(g), 1, _lib.i64_array([0, p.numel()]),
             _lib.f64_array([lr]), _lib.f64_array([-math.inf]),
-            _lib.stream()), "pc_sgd_segments")
+            _lib.stream()), "pc_sgd_segments_f64")
     _inplace(param, p)
 
 

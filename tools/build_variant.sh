@@ -9,6 +9,9 @@ OUT=$ROOT/build/variants/$NAME
 mkdir -p $OUT
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include $DEFS"
-nvcc $FL -Xptxas -v -c $C/radiator.cu -o $OUT/radiator.o 2>&1 | grep -A2 "k_forwardILb0ELb0E\|k_adjointILb1" | grep -E "registers|spill" || true
-nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/$NAME.so $OUT/radiator.o $C/deform.o $C/optim.o $C/voxel.o $C/ubp.o
+for f in radiator fwd_run deform optim voxel ubp; do
+  nvcc $FL -c $C/$f.cu -o $OUT/$f.o &
+done
+wait
+nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/$NAME.so $OUT/*.o
 echo built build/variants/$NAME.so

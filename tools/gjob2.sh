@@ -1,0 +1,13 @@
+# new forward: smoke, parity per config (new vs legacy), GPU tests, A/B bench configs 2,3
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/j2_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/j2_smoke.log
+for c in 1 2 3 5 4; do
+  timeout 300 python tools/check_fwd_config.py $c 16 >> gpurun_out/j2_parity.log 2>&1
+  PC_FWD_LEGACY=1 timeout 300 python tools/check_fwd_config.py $c 16 >> gpurun_out/j2_parity_legacy.log 2>&1
+done
+timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/j2_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/j2_pytest.log
+for c in 2 3; do
+  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/j2_bench$c.log 2>&1
+  PC_FWD_LEGACY=1 timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/j2_bench${c}_legacy.log 2>&1
+done
+echo done
