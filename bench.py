@@ -1,5 +1,6 @@
 """Benchmark: BASELINE metric "ball x sensor pair-evals/s (fwd+adjoint) and
-iteration ms" on BASELINE config 2 (default; `--config` selects others).
+iteration ms" on BASELINE config 3 (default: the largest single-GPU config and
+the BASELINE's frame-sharded 1/2/4/8-GPU case; `--config` selects others).
 
 One step = one full 4D iteration through the fused engine: deform ->
 forward + residual + L2 loss -> adjoint -> deformation backward ->
@@ -41,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -169,66 +170,118 @@ def support_samples_torch(mu_t, a0_t, pos, v, t0, dt, T, support=6.0):
     return total
 
 
-def cpu_reference_sample(prob, n_sensors, threads):
-    """Oracle fwd+adjoint on a bounded sample: frame 0 (deformed states),
-    every k-th sensor, all balls.  Returns (pair-evals/s, desc, cores)."""
+def full_support_initial(prob, dev):
+    """Sum over every (ball, sensor, frame) of the in-support window length
+    for the problem's initial cloud (the states the CPU sample is drawn
+    from), counted on the device (measurement plumbing; states from the
+    oracle's deformation restatement)."""
     import oracle
-    from paper_2412_03898_b200.core import SensorArray
+    import torch
     cfg = prob.config
-    st = oracle.cloud_states_at(prob.cloud, float(prob.frame_times[0]),
-                                cfg.coord_mode, cfg.a0_floor,
-                                basis=prob.cloud.basis)
-    M = prob.array.n_sensors
-    step = max(1, M // max(1, n_sensors))
-    sel = np.arange(0, M, step)[:n_sensors]
-    sub = SensorArray(prob.array.positions[sel], prob.array.sound_speed,
-                      prob.array.sample_rate, prob.array.n_samples,
-                      prob.array.t_start)
-    a, p, m = prob.gt_frames[0]
-    obs = oracle.forward_frame(oracle.States(a, p, m), sub, threads=threads)
-    oracle.forward_frame(st, sub, threads=threads)      # warm caches
-    best = math.inf
-    for _ in range(2):
+    pos = torch.as_tensor(prob.array.positions, dtype=torch.float64,
+                          device=dev)
+    dt = 1.0 / prob.array.sample_rate
+    total = 0
+    for t in prob.frame_times:
+        st = oracle.cloud_states_at(prob.cloud, float(t), cfg.coord_mode,
+                                    cfg.a0_floor, basis=prob.cloud.basis)
+        total += support_samples_torch(
+            torch.as_tensor(st.mu_t, device=dev)[None],
+            torch.as_tensor(st.a0_t, device=dev)[None], pos,
+            prob.array.sound_speed, prob.array.t_start, dt,
+            prob.array.n_samples, cfg.support_sigmas)
+    return total
+
+
+class CpuSample:
+    """The reference algorithm's CPU port (oracle/, the C restatement of the
+    numba kernels radiator.py:86-174) on a bounded, deterministic sample of
+    one iteration: frame 0 (deformed states), every k-th sensor, all balls,
+    forward + adjoint in fp64 on `threads` host threads.  The full
+    iteration's time is extrapolated by in-support samples (SURVEY.md 8d:
+    the port's cost is linear in the window samples), so `value` is the
+    pair-evals/s the port would reach on the whole iteration."""
+
+    def __init__(self, prob, n_sensors, threads, full_support=None):
+        import oracle
+        from paper_2412_03898_b200.core import SensorArray
+        cfg = prob.config
+        self.threads = threads
+        self.st = oracle.cloud_states_at(prob.cloud, float(prob.frame_times[0]),
+                                         cfg.coord_mode, cfg.a0_floor,
+                                         basis=prob.cloud.basis)
+        M = prob.array.n_sensors
+        step = max(1, M // max(1, n_sensors))
+        sel = np.arange(0, M, step)[:n_sensors]
+        self.sub = SensorArray(prob.array.positions[sel],
+                               prob.array.sound_speed, prob.array.sample_rate,
+                               prob.array.n_samples, prob.array.t_start)
+        a, p, m = prob.gt_frames[0]
+        self.obs = oracle.forward_frame(oracle.States(a, p, m), self.sub,
+                                        threads=threads)
+        self.s_sample = oracle.support_samples(self.st, self.sub,
+                                               cfg.support_sigmas,
+                                               threads=threads)
+        shp = prob.meta["shape"]
+        self.pairs_full = shp["B"] * shp["M"] * shp["F"]
+        if full_support is None:
+            full_support = 0
+            for k in range(shp["F"]):
+                stk = oracle.cloud_states_at(
+                    prob.cloud, float(prob.frame_times[k]), cfg.coord_mode,
+                    cfg.a0_floor, basis=prob.cloud.basis)
+                full_support += oracle.support_samples(
+                    stk, prob.array, cfg.support_sigmas, threads=threads)
+        self.s_full = int(full_support)
+        self.desc = (f"frame 0, {len(sel)} of {M} sensors (every {step}th), "
+                     f"all {len(self.st.a0_t)} balls: oracle fwd+adjoint "
+                     f"fp64 on {threads} threads; extrapolated to the full "
+                     f"iteration by in-support samples "
+                     f"({self.s_full:.4e} / {self.s_sample:.4e})")
+
+    def time_once(self):
+        import oracle
         t = time.perf_counter()
-        pred = oracle.forward_frame(st, sub, threads=threads)
-        oracle.frame_state_grads(st, sub, pred - obs, threads=threads)
-        best = min(best, time.perf_counter() - t)
-    pairs = len(st.a0_t) * len(sel)
-    desc = (f"frame 0, {len(sel)} of {M} sensors (every {step}th), all "
-            f"{len(st.a0_t)} balls; oracle fwd+adjoint fp64, min of 2")
-    return pairs / best, desc, best
+        pred = oracle.forward_frame(self.st, self.sub, threads=self.threads)
+        oracle.frame_state_grads(self.st, self.sub, pred - self.obs,
+                                 threads=self.threads)
+        return time.perf_counter() - t
+
+    def value(self, secs):
+        """pair-evals/s of the whole iteration extrapolated from `secs`."""
+        return self.pairs_full / (secs * self.s_full / self.s_sample)
 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm's CPU port (the reference
-    is pure Python/numba; its C restatement in oracle/ is timed)."""
+    is pure Python/numba; its C restatement in oracle/ is timed), each step
+    one bounded sample of the iteration, extrapolated by in-support
+    samples."""
     if rank != 0:
         return
-    import oracle
     from paper_2412_03898_b200 import synth
     prob = synth.make_problem(args.config, seed=args.seed)
     threads = os.cpu_count() or 1
     n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
-    vals = []
-    desc = ""
+    samp = CpuSample(prob, n_s, threads)
     for _ in range(max(1, args.warmup)):
-        cpu_reference_sample(prob, n_s, threads)
+        samp.time_once()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, desc, _ = cpu_reference_sample(prob, n_s, threads)
-        vals.append(v)
+    secs = [samp.time_once() for _ in range(args.steps)]
     wall = time.perf_counter() - t0
-    value = float(np.median(vals))
-    shp = prob.meta["shape"]
+    value = samp.value(float(np.median(secs)))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * shp["B"] * shp["M"] * shp["F"] / value,
+        "ms_per_step": 1e3 * samp.pairs_full / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, fp32-quantised)",
         "config": workload_config(args.config, prob, world),
+        "extrapolated": True,
         "cpu_baseline": {"value": value, "unit": UNIT,
-                         "cores": threads, "kind": "port", "sample": desc},
+                         "cores": threads, "kind": "port",
+                         "sample": samp.desc, "extrapolated": True,
+                         "sample_s_median": float(np.median(secs))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": wall,
@@ -396,7 +449,7 @@ def run_ours(args, rank, world, local):
     roofline = {
         "bound": "fp32", "unit": "TFLOP/s", "achieved": achieved,
         "peak": peak, "frac": achieved / peak, "traffic": traffic,
-        "kernel": "k_forward + k_adjoint (fwd+adj per local shard)",
+        "kernel": "k_fwd_run + k_adjoint (every forward and adjoint launch of one iteration on the local shard)",
         "flops_per_launch": FLOPS_PER_SAMPLE * S,
         "support_samples": S, "t_fwd_ms": t_fwd, "t_adj_ms": t_adj,
         "kernel_pair_evals_per_s": kern_pairs / ((t_fwd + t_adj) * 1e-3),
@@ -466,9 +519,13 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
-        v, desc, secs = cpu_reference_sample(prob, n_s, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": desc}
+        samp = CpuSample(prob, n_s, threads,
+                         full_support=full_support_initial(prob, dev))
+        samp.time_once()
+        secs = min(samp.time_once() for _ in range(2))
+        cpu = {"value": samp.value(secs), "unit": UNIT, "cores": threads,
+               "kind": "port", "sample": samp.desc + ", min of 2",
+               "extrapolated": True}
 
     # deform + forward[+combine]+loss-reduce + adjoint + deform-bwd + finite
     # guard + Adam

@@ -93,3 +93,57 @@ def test_small_grid_sensor_split_adjoint(pc):
     g = G1[0].double().cpu().numpy()
     for c in range(5):
         assert rel_l2(g[:, c], g_ref[:, c]) < GRAD_TOL, c
+
+
+def _subarray(arr, every):
+    from paper_2412_03898_b200.core import SensorArray
+    return SensorArray(arr.positions[::every], arr.sound_speed,
+                       arr.sample_rate, arr.n_samples, arr.t_start)
+
+
+def test_config3_full_iteration_vs_oracle(pc):
+    """One full BASELINE config-3 engine iteration — all 200,000 balls, all
+    32 frames, poly+Fourier deformation, forward + loss + adjoint + fused
+    deformation backward — against the oracle's frame loop
+    (reconstruction.py:293-316) on a 16-sensor subsample of the 1,024."""
+    from paper_2412_03898_b200 import synth
+    from paper_2412_03898_b200.engine import IterationEngine
+    from paper_2412_03898_b200.radiator import DeviceArray, forward_device
+    prob = synth.make_problem(3)
+    sub = _subarray(prob.array, 64)
+    darr = DeviceArray(sub, 6.0, False)
+    obs = []
+    for a, p, m in prob.gt_frames:          # observed traces (input only)
+        mm, aa, pp = _dev(m, a, p)
+        obs.append(forward_device(darr, mm, aa, pp)[0][0].cpu().numpy())
+    obs = np.stack(obs).astype(np.float32)
+    frames = np.arange(prob.n_frames)
+    eng = IterationEngine(prob.cloud, sub, obs, prob.frame_times, prob.config)
+    eng.compute_grads(frames)
+    loss, flags, _ = eng.check_and_status()
+    g = eng.grads_numpy()
+    ref_loss, ref = oracle.iteration_grads(
+        prob.cloud, prob.frame_times, obs.astype(np.float64), sub,
+        prob.config, basis=prob.cloud.basis)
+    assert not flags.any()
+    assert abs(loss - ref_loss) / ref_loss < SIGNAL_TOL
+    for k in ("p0", "a0", "mu", "omega"):
+        assert rel_l2(g[k], getattr(ref, k)) < GRAD_TOL, k
+
+
+def test_config4_forward_256_sensors_adjoint_64(pc):
+    """BASELINE config 4 (1,000,000 balls, 60 mm hemisphere, T = 8192):
+    forward on 256 of the 2,048 sensors and adjoint on 64, full cloud."""
+    arr, sub, a0, p0, mu = _frame(4, 8)
+    st = oracle.States(a0, p0, mu)
+    ref = oracle.forward_frame(st, sub)
+    got = pc.forward_frame(pc.CloudState(a0, p0, mu), sub)
+    assert rel_l2(got, ref) < SIGNAL_TOL
+    sub64 = _subarray(arr, 32)
+    rng = np.random.default_rng(44)
+    res = rng.normal(0, 1e-2, (64, arr.n_samples))
+    res = res.astype(np.float32).astype(np.float64)
+    g_ref = oracle.frame_state_grads(st, sub64, res)
+    g = pc.frame_state_grads(pc.CloudState(a0, p0, mu), sub64, res)
+    for c in range(5):
+        assert rel_l2(g[:, c], g_ref[:, c]) < GRAD_TOL, c
