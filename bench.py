@@ -52,6 +52,12 @@ def parse():
                     help="config 5: densify/prune every N iterations")
     ap.add_argument("--max-balls", type=int, default=500000,
                     help="config 5: growth cap")
+    ap.add_argument("--basis", default="polyfourier",
+                    choices=["polyfourier", "gauss"],
+                    help="deformation basis: BASELINE's poly+Fourier (N=8) "
+                         "or the reference default Gaussian basis")
+    ap.add_argument("--n-basis", type=int, default=None,
+                    help="Gaussian basis size (reference default 65)")
     return ap.parse_args()
 
 
@@ -260,7 +266,8 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_2412_03898_b200 import synth
-    prob = synth.make_problem(args.config, seed=args.seed)
+    prob = synth.make_problem(args.config, seed=args.seed, basis=args.basis,
+                              n_basis=args.n_basis)
     threads = os.cpu_count() or 1
     n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
     samp = CpuSample(prob, n_s, threads)
@@ -321,7 +328,8 @@ def run_ours(args, rank, world, local):
         kw = {"device_id": dev} if backend == "nccl" else {}
         torch.distributed.init_process_group(
             backend, timeout=datetime.timedelta(minutes=10), **kw)
-    prob = synth.make_problem(args.config, seed=args.seed)
+    prob = synth.make_problem(args.config, seed=args.seed, basis=args.basis,
+                              n_basis=args.n_basis)
     shp = prob.meta["shape"]
     B, M, T, F = shp["B"], shp["M"], shp["T"], shp["F"]
     arr = prob.array
@@ -363,11 +371,14 @@ def run_ours(args, rank, world, local):
         if world > 1:
             torch.distributed.barrier()
 
+    growth = []
+
     def step(it):
         """One iteration (+ the config-5 densify/prune when due)."""
         eng.iterate(it, frames_all)
         if args.config == 5 and (it + 1) % args.densify_every == 0:
             eng.densify(p0_min=0.01, q=90.0, max_balls=args.max_balls)
+            growth.append((it, eng.B))
 
     for _ in range(args.warmup):
         step(it)
@@ -546,6 +557,25 @@ def run_ours(args, rank, world, local):
             "final_loss": float(eng.loss_total.item()),
             "final_balls": int(eng.B),
         }
+        if args.config == 5:
+            # per-step times: densify steps (prune/split + gathers; the next
+            # step re-captures the graphs at the new ball count) vs the rest
+            first = args.warmup
+            dens = {i - first for i, _ in growth if i >= first}
+            after = {i + 1 for i in dens}
+            plain = [t for i, t in enumerate(step_ms)
+                     if i not in dens and i not in after]
+            line["growth"] = {
+                "densify_every": args.densify_every,
+                "balls_at_densify": [b for _, b in growth],
+                "step_ms_plain_mean": float(np.mean(plain)) if plain else None,
+                "step_ms_densify_mean": float(np.mean(
+                    [step_ms[i] for i in dens])) if dens else None,
+                "step_ms_after_densify_mean": float(np.mean(
+                    [step_ms[i] for i in after if i < len(step_ms)]))
+                if after else None,
+                "step_ms": [round(t, 3) for t in step_ms]
+                if len(step_ms) <= 400 else None}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -333,12 +333,34 @@ int pc_compact_index(const uint8_t *keep, const uint8_t *append,
  * reference has pruning only, reconstruction.py:217-226):
  *   keep[b]  = !(p0[b] < p0_min)
  *   split[b] = keep[b] && |g[b]| > threshold       (g = dL/dp0, f32)
- * `threshold` is the numpy 'linear' percentile of |g| (computed by the host
- * from device order statistics).  counts (device int64[2]) receive
- * (#keep, #split). */
+ * `threshold` (device double) is the numpy 'linear' percentile of |g|
+ * (pc_abs_quantile_f32).  counts (device int64[2]) receive (#keep, #split). */
 int pc_densify_masks(const double *p0, const float *g, int64_t n_balls,
-                     double p0_min, double threshold, uint8_t *keep,
+                     double p0_min, const double *threshold, uint8_t *keep,
                      uint8_t *split, int64_t *counts, pc_stream_t stream);
+
+/* Workspace bytes of pc_abs_quantile_f32 (independent of n). */
+size_t pc_abs_quantile_workspace_bytes(void);
+
+/* numpy.percentile(|g|, q, method='linear') of a device f32 array, on the
+ * device (no host round trip): the caller passes numpy's virtual-index
+ * split k = floor((n-1) q/100), gamma = (n-1) q/100 - k (0 <= gamma < 1,
+ * k < n); the order statistics x_(k), x_(k+1) of |g| come from a radix
+ * select and are combined by numpy's _lerp
+ * (numpy/lib/_function_base_impl.py) in round-to-nearest fp64.  The result
+ * is written to *threshold (device double).  g must be finite. */
+int pc_abs_quantile_f32(const float *g, int64_t n, int64_t k, double gamma,
+                        double *threshold, void *workspace,
+                        size_t workspace_bytes, pc_stream_t stream);
+
+/* Densify flags after pc_compact_index(keep, split) (index[0, n_keep) =
+ * survivors, index[n_keep, n_out) = children's parents, n_out possibly
+ * truncated by a ball cap): child[i] = i >= n_keep; halve[i] = child[i] or
+ * survivor i's child is in [n_keep, n_out).  has_child: scratch of n_balls
+ * bytes. */
+int pc_densify_flags(const int64_t *index, int64_t n_balls, int64_t n_keep,
+                     int64_t n_out, uint8_t *has_child, uint8_t *halve,
+                     uint8_t *child, pc_stream_t stream);
 
 /* After the gather of a densify step (new order = survivors then children):
  * p0[i] *= 0.5 where halve[i] (split parents and their children) and

@@ -461,7 +461,7 @@ def percentile_linear(x, q):
     return float(np.percentile(x, q))
 
 
-def densify_plan(p0, gp0, p0_min=0.01, q=90.0):
+def densify_plan(p0, gp0, p0_min=0.01, q=90.0, max_balls=None):
     """Config-5 rule (builder-defined, unpinned).
 
     prune: p0 < p0_min (strict); split: |gp0| > P_q(|gp0|) (strict, numpy
@@ -476,6 +476,11 @@ def densify_plan(p0, gp0, p0_min=0.01, q=90.0):
     split = (g > thr) & keep
     survivors = np.nonzero(keep)[0]
     children = np.nonzero(split)[0]
+    if max_balls is not None:
+        # cap: the first (max_balls - #survivors) split balls, parent order
+        children = children[:max(0, int(max_balls) - len(survivors))]
+        split = np.zeros_like(split)
+        split[children] = True
     index = np.concatenate([survivors, children]).astype(np.int64)
     is_child = np.concatenate([np.zeros(len(survivors), bool),
                                np.ones(len(children), bool)])

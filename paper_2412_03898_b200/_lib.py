@@ -111,8 +111,13 @@ SIGNATURES = {
                                 _P]),
     "pc_compact_index": (c_int32, [_P, _P, c_int64, _P, _P, _P, c_size_t,
                                    _P]),
-    "pc_densify_masks": (c_int32, [_P, _P, c_int64, c_double, c_double, _P,
+    "pc_densify_masks": (c_int32, [_P, _P, c_int64, c_double, _P, _P,
                                    _P, _P, _P]),
+    "pc_abs_quantile_workspace_bytes": (c_size_t, []),
+    "pc_abs_quantile_f32": (c_int32, [_P, c_int64, c_int64, c_double, _P, _P,
+                                      c_size_t, _P]),
+    "pc_densify_flags": (c_int32, [_P, c_int64, c_int64, c_int64, _P, _P, _P,
+                                   _P]),
     "pc_densify_apply": (c_int32, [_P, _P, _P, _P, _P, c_int64, c_double,
                                    _P]),
     "pc_gather_rows": (c_int32, [_P, _P, _P, c_int64, c_int64, _P]),

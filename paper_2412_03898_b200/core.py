@@ -164,6 +164,13 @@ class DeformField:
     def shared_basis(self) -> bool:
         return self.theta.ndim == 1
 
+    @classmethod
+    def identity(cls, n_basis: int) -> "DeformField":
+        """Zero weights over the default theta grid: H(t) = 0 everywhere
+        (reference core.py:145-149)."""
+        theta, sigma = default_basis_grid(n_basis)
+        return cls(theta, sigma, np.zeros((N_CHANNELS, n_basis)))
+
 
 @dataclass(frozen=True)
 class Violation:

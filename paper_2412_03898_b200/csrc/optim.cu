@@ -8,6 +8,10 @@
 //   pc_prune_mask       <- reconstruction.py:217-220 (keep = p0 > thr*max p0)
 //   pc_compact_index    <- reconstruction.py:95-100 (stable boolean gather)
 //   pc_gather_rows      <- the gather itself, for params and Adam moments
+//   pc_abs_quantile_f32 <- config-5 densify threshold: numpy.percentile(|g|,
+//                          q, 'linear') by device radix select (builder rule)
+//   pc_densify_masks / pc_densify_flags / pc_densify_apply <- config-5 split
+//                          + absolute prune (builder-defined)
 #include <math.h>
 
 #include "common.cuh"
@@ -257,11 +261,13 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ src
 
 __global__ void __launch_bounds__(256) k_densify_masks(const double* __restrict__ p0,
                                                        const float* __restrict__ g, int64_t n,
-                                                       double p0_min, double thr,
+                                                       double p0_min,
+                                                       const double* __restrict__ thr_dev,
                                                        uint8_t* __restrict__ keep,
                                                        uint8_t* __restrict__ split,
                                                        unsigned long long* __restrict__ counts) {
     (void)counts;
+    const double thr = *thr_dev;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t k = (p0[i] < p0_min) ? 0 : 1;
@@ -291,6 +297,135 @@ __global__ void __launch_bounds__(256) k_count_u8(const uint8_t* __restrict__ a,
     }
 }
 
+
+// ------------------------------------------------ order statistic of |g|
+// numpy.percentile(|g|, q, method='linear') on the device (config-5 densify
+// threshold; numpy/lib/_function_base_impl.py _quantile + _lerp): the host
+// passes numpy's virtual-index split k = floor((n-1) q), gamma = (n-1) q - k
+// (it depends on n and q only); the device finds the order statistics
+// x_(k), x_(k+1) of |g| by an MSB-first 8-bit radix select on the float
+// bit patterns (non-negative floats order like their uint32 bits) and
+// applies numpy's lerp with explicit round-to-nearest double operations.
+
+struct QuantState {
+    unsigned int prefix;     // selected high digits of x_(k)
+    unsigned int mask;       // digits fixed so far
+    long long rank;          // rank of x_(k) among the elements matching prefix
+    unsigned int a_bits;     // x_(k) when done
+    unsigned int min_gt;     // min |g| > x_(k)      (atomicMin)
+    unsigned long long n_le; // #{|g| <= x_(k)}       (atomicAdd)
+};
+
+__device__ __forceinline__ unsigned int abs_bits(float x) {
+    return __float_as_uint(x) & 0x7fffffffu;
+}
+
+__global__ void __launch_bounds__(256) k_radix_hist(const float* __restrict__ g, int64_t n,
+                                                    const QuantState* __restrict__ st,
+                                                    int shift,
+                                                    unsigned int* __restrict__ hist) {
+    __shared__ unsigned int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned int prefix = st->prefix, mask = st->mask;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned int u = abs_bits(g[i]);
+        if ((u & mask) == prefix) atomicAdd(&h[(u >> shift) & 0xffu], 1u);
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// one block of 256: pick the digit holding `rank`, clear the histogram
+__global__ void __launch_bounds__(256) k_radix_pick(QuantState* __restrict__ st, int shift,
+                                                    unsigned int* __restrict__ hist) {
+    __shared__ unsigned int c[256];
+    const int t = threadIdx.x;
+    c[t] = hist[t];
+    hist[t] = 0;
+    __syncthreads();
+    // inclusive scan (Hillis-Steele; 256 entries)
+    for (int o = 1; o < 256; o <<= 1) {
+        const unsigned int v = t >= o ? c[t - o] : 0u;
+        __syncthreads();
+        c[t] += v;
+        __syncthreads();
+    }
+    const long long r = st->rank;
+    const unsigned long long lo = t ? c[t - 1] : 0u;
+    if ((long long)lo <= r && r < (long long)c[t]) {
+        st->prefix |= (unsigned int)t << shift;
+        st->mask |= 0xffu << shift;
+        st->rank = r - (long long)lo;
+        if (shift == 0) {
+            st->a_bits = st->prefix;
+            st->min_gt = 0x7f800000u;   // +inf
+            st->n_le = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_quant_next(const float* __restrict__ g, int64_t n,
+                                                    QuantState* __restrict__ st) {
+    const unsigned int a = st->a_bits;
+    unsigned int mn = 0x7f800000u;
+    unsigned long long le = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned int u = abs_bits(g[i]);
+        if (u <= a) ++le;
+        else mn = min(mn, u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        le += __shfl_xor_sync(0xffffffffu, le, o);
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&st->n_le, le);
+        atomicMin(&st->min_gt, mn);
+    }
+}
+
+__global__ void k_quant_lerp(const QuantState* __restrict__ st, int64_t k, int64_t n,
+                             double gamma, double* __restrict__ out) {
+    const double a = (double)__uint_as_float(st->a_bits);
+    // x_(k+1): x_(k) again while more than k+1 elements are <= x_(k)
+    const bool same = k + 1 >= n || (long long)st->n_le > k + 1;
+    const double b = same ? a : (double)__uint_as_float(st->min_gt);
+    const double diff = __dsub_rn(b, a);
+    // numpy _lerp: a + diff*t, replaced by b - diff*(1-t) where t >= 0.5
+    out[0] = gamma >= 0.5 ? __dsub_rn(b, __dmul_rn(diff, __dsub_rn(1.0, gamma)))
+                          : __dadd_rn(a, __dmul_rn(diff, gamma));
+}
+
+// ------------------------------------------------ densify flags
+// After pc_compact_index(keep, split): index[0, n_keep) survivors,
+// index[n_keep, n_out) children (parent ids).  has_child[b] marks parents
+// whose child made it into [n_keep, n_out) (a max-balls cap truncates the
+// children); halve[i] = parent of a child, or a child; child[i] = i >= n_keep.
+__global__ void __launch_bounds__(256) k_mark_parents(const int64_t* __restrict__ index,
+                                                      int64_t n_keep, int64_t n_out,
+                                                      uint8_t* __restrict__ has_child) {
+    for (int64_t r = n_keep + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_out;
+         r += (int64_t)gridDim.x * blockDim.x)
+        has_child[index[r]] = 1;
+}
+
+__global__ void __launch_bounds__(256) k_densify_flags(const int64_t* __restrict__ index,
+                                                       int64_t n_keep, int64_t n_out,
+                                                       const uint8_t* __restrict__ has_child,
+                                                       uint8_t* __restrict__ halve,
+                                                       uint8_t* __restrict__ child) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_out;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool c = i >= n_keep;
+        child[i] = c ? 1 : 0;
+        halve[i] = (c || has_child[index[i]]) ? 1 : 0;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_densify_apply(double* __restrict__ p0,
                                                        double* __restrict__ mu,
                                                        const double* __restrict__ a0,
@@ -308,14 +443,62 @@ __global__ void __launch_bounds__(256) k_densify_apply(double* __restrict__ p0,
 
 using namespace pc;
 
+extern "C" size_t pc_abs_quantile_workspace_bytes(void) {
+    return sizeof(QuantState) + 256 * sizeof(unsigned int) + 64;
+}
+
+extern "C" int pc_abs_quantile_f32(const float* g, int64_t n, int64_t k, double gamma,
+                                   double* threshold, void* workspace, size_t workspace_bytes,
+                                   pc_stream_t stream) {
+    if (n < 1 || k < 0 || k >= n || !(gamma >= 0.0 && gamma < 1.0) || !g || !threshold ||
+        !workspace || workspace_bytes < pc_abs_quantile_workspace_bytes())
+        return PC_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    QuantState* qs = reinterpret_cast<QuantState*>(workspace);
+    unsigned int* hist = reinterpret_cast<unsigned int*>(
+        reinterpret_cast<char*>(workspace) + ((sizeof(QuantState) + 63) / 64) * 64);
+    QuantState init{};
+    init.rank = k;
+    if (cudaMemcpyAsync(qs, &init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), st) != cudaSuccess)
+        return PC_ERR_CUDA;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4LL * num_sms()) blocks = 4LL * num_sms();
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        k_radix_hist<<<(unsigned)blocks, 256, 0, st>>>(g, n, qs, shift, hist);
+        k_radix_pick<<<1, 256, 0, st>>>(qs, shift, hist);
+    }
+    k_quant_next<<<(unsigned)blocks, 256, 0, st>>>(g, n, qs);
+    k_quant_lerp<<<1, 1, 0, st>>>(qs, k, n, gamma, threshold);
+    return last_status();
+}
+
+extern "C" int pc_densify_flags(const int64_t* index, int64_t n_balls, int64_t n_keep,
+                                int64_t n_out, uint8_t* has_child, uint8_t* halve,
+                                uint8_t* child, pc_stream_t stream) {
+    if (n_balls < 0 || n_keep < 0 || n_out < n_keep || n_out > 2 * n_balls)
+        return PC_ERR_ARGUMENT;
+    if (n_out == 0) return PC_OK;
+    if (!index || !has_child || !halve || !child) return PC_ERR_ARGUMENT;
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemsetAsync(has_child, 0, (size_t)n_balls, st) != cudaSuccess) return PC_ERR_CUDA;
+    int64_t blocks = (n_out + 255) / 256;
+    if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+    if (n_out > n_keep)
+        k_mark_parents<<<(unsigned)blocks, 256, 0, st>>>(index, n_keep, n_out, has_child);
+    k_densify_flags<<<(unsigned)blocks, 256, 0, st>>>(index, n_keep, n_out, has_child, halve,
+                                                      child);
+    return last_status();
+}
+
 extern "C" int pc_densify_masks(const double* p0, const float* g, int64_t n_balls, double p0_min,
-                                double threshold, uint8_t* keep, uint8_t* split, int64_t* counts,
-                                pc_stream_t stream) {
+                                const double* threshold, uint8_t* keep, uint8_t* split,
+                                int64_t* counts, pc_stream_t stream) {
     if (n_balls < 0 || !counts) return PC_ERR_ARGUMENT;
     cudaStream_t st = as_stream(stream);
     if (cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), st) != cudaSuccess) return PC_ERR_CUDA;
     if (n_balls == 0) return PC_OK;
-    if (!p0 || !g || !keep || !split) return PC_ERR_ARGUMENT;
+    if (!p0 || !g || !keep || !split || !threshold) return PC_ERR_ARGUMENT;
     int64_t blocks = (n_balls + 255) / 256;
     if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
     k_densify_masks<<<(unsigned)blocks, 256, 0, st>>>(p0, g, n_balls, p0_min, threshold, keep,

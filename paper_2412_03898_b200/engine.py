@@ -186,6 +186,11 @@ class IterationEngine:
         self.dcloud = DeviceCloud(p["p0"], p["a0"], p["mu"], p.get("theta"),
                                   p.get("sigma"), p["omega"], self.basis)
         self.use_graph = bool(use_graph)
+        # per-stage CUDA-event timings of each iterate() (progress records)
+        self.stage_timing = os.environ.get("PC_STAGE_TIMING", "0") == "1"
+        self.last_timing = None
+        self._events = None
+        self._qws = None            # pc_abs_quantile_f32 workspace (densify)
         self._warmed = False
         self._graph = None
         self._graph_frames = None
@@ -582,10 +587,38 @@ class IterationEngine:
         updates the reference makes before raising)."""
         lrs = self._lrs(iteration)
         self.last_lrs = lrs
+        nvtx = torch.cuda.nvtx
+        ev = self._stage_events() if self.stage_timing else None
+        if ev:
+            ev[0].record()
+        nvtx.range_push("pc:grads (deform, forward+loss, adjoint, deform-bwd)")
         self.compute_grads(frames)
+        nvtx.range_pop()
+        if ev:
+            ev[1].record()
+        nvtx.range_push("pc:exchange")
         self.allreduce()
+        nvtx.range_pop()
+        if ev:
+            ev[2].record()
+        nvtx.range_push("pc:guard+adam")
         self._guarded_update(lrs)
+        nvtx.range_pop()
+        if ev:
+            ev[3].record()
+        nvtx.range_push("pc:status (host sync)")
         loss, flags, coinc = self._status()
+        nvtx.range_pop()
+        if ev:
+            # every event completed before the status read returned
+            n_loc = len(self._local_frames(frames))
+            grads = ev[0].elapsed_time(ev[1])
+            self.last_timing = {
+                "grads_ms": grads, "exchange_ms": ev[1].elapsed_time(ev[2]),
+                "update_ms": ev[2].elapsed_time(ev[3]),
+                "iteration_ms": ev[0].elapsed_time(ev[3]),
+                "pair_evals_per_s": self.B * self.darr.M * n_loc /
+                (grads * 1e-3) if grads > 0 else None}
         if coinc != _lib.INT64_MAX:
             self._raise_coincident(coinc, frames)
         if not math.isfinite(loss):
@@ -603,6 +636,12 @@ class IterationEngine:
             raise ValueError(
                 f"non-finite gradient in parameter group '{segs[bad].group}'")
         return loss
+
+    def _stage_events(self):
+        if self._events is None:
+            self._events = [torch.cuda.Event(enable_timing=True)
+                            for _ in range(4)]
+        return self._events
 
     def _raise_coincident(self, word: int, frames) -> None:
         """reconstruction.py:303-311 -> radiator.py:186-192: the first frame
@@ -627,59 +666,66 @@ class IterationEngine:
                             self.positions_all)
 
     # ------------------------------------------------------------ densify
-    def p0_grad_threshold(self, q: float = 90.0) -> float:
-        """numpy.percentile(|dL/dp0|, q, method='linear') of the last
-        computed gradient: device sort (order statistics), then numpy's own
-        index / lerp arithmetic (numpy/lib/_function_base_impl.py _lerp) on
-        the two neighbours, in float64 on the host."""
-        g = self.grads["p0"].abs().double()
-        n = int(g.numel())
-        if n == 0:
-            return 0.0
-        srt = torch.sort(g).values
+    @staticmethod
+    def _percentile_split(n: int, q: float):
+        """numpy's 'linear' virtual index (n - 1) q / 100 split into the
+        lower order-statistic rank k and the lerp weight gamma
+        (numpy/lib/_function_base_impl.py _quantile); host arithmetic on n
+        and q only."""
         qq = float(np.float64(q) / np.float64(100.0))
         virtual = (n - 1) * qq
         if virtual >= n - 1:
-            return float(srt[-1].item())
-        if virtual < 0:
-            return float(srt[0].item())
-        prev = math.floor(virtual)
-        gamma = virtual - prev
-        ab = srt[prev:prev + 2].cpu().numpy()
-        a, b = float(ab[0]), float(ab[1])
-        diff = b - a
-        return b - diff * (1.0 - gamma) if gamma >= 0.5 else a + diff * gamma
+            return n - 1, 0.0
+        k = max(0, math.floor(virtual))
+        return k, virtual - k
+
+    def _p0_grad_threshold_dev(self, q: float) -> torch.Tensor:
+        """Device double: numpy.percentile(|dL/dp0|, q, method='linear') of
+        the last computed gradient (pc_abs_quantile_f32: radix select +
+        numpy's _lerp on the device, no host round trip)."""
+        lib = _lib.load_library()
+        n = int(self.B)
+        thr = torch.zeros(1, dtype=torch.float64, device=self.device)
+        if n == 0:
+            return thr
+        k, gamma = self._percentile_split(n, q)
+        if self._qws is None:
+            self._qws = torch.empty(int(lib.pc_abs_quantile_workspace_bytes()),
+                                    dtype=torch.uint8, device=self.device)
+        _lib.check(lib.pc_abs_quantile_f32(
+            _lib.ptr(self.grads["p0"]), n, int(k), float(gamma), _lib.ptr(thr),
+            _lib.ptr(self._qws), self._qws.numel(), _lib.stream()),
+            "pc_abs_quantile_f32")
+        return thr
+
+    def p0_grad_threshold(self, q: float = 90.0) -> float:
+        """numpy.percentile(|dL/dp0|, q, method='linear'), read back."""
+        return float(self._p0_grad_threshold_dev(q).item())
 
     def densify(self, p0_min: float = 0.01, q: float = 90.0,
                 child_shift: float = 0.5, max_balls: int | None = None):
         """Config-5 adaptive step (builder-defined): prune
         p0 < p0_min, split balls with |dL/dp0| above its q-th percentile.
         New order = survivors in order, then one child per split survivor in
-        parent order (pc_compact_index); every parameter and Adam moment is
-        gathered (pc_gather_rows, step counts preserved as in
-        reconstruction.py:95-100); split parents and children get half the
-        pressure and children move +child_shift*a0 along x
-        (pc_densify_apply); children start with zero moments.
+        parent order (pc_compact_index), truncated to `max_balls`; every
+        parameter and Adam moment is gathered (pc_gather_rows, step counts
+        preserved as in reconstruction.py:95-100); split parents and
+        children get half the pressure and children move +child_shift*a0
+        along x (pc_densify_flags + pc_densify_apply); children start with
+        zero moments.  Everything runs on the device; the one host read is
+        the (#keep, #split) pair that sizes the new cloud.
         Returns (n_pruned, n_children)."""
         lib = _lib.load_library()
         B = self.B
         dev = self.device
-        thr = self.p0_grad_threshold(q)
+        thr = self._p0_grad_threshold_dev(q)
         keep = torch.empty(B, dtype=torch.uint8, device=dev)
         split = torch.empty(B, dtype=torch.uint8, device=dev)
         counts = torch.zeros(2, dtype=torch.int64, device=dev)
         _lib.check(lib.pc_densify_masks(
             _lib.ptr(self.params["p0"]), _lib.ptr(self.grads["p0"]), B,
-            float(p0_min), float(thr), _lib.ptr(keep), _lib.ptr(split),
+            float(p0_min), _lib.ptr(thr), _lib.ptr(keep), _lib.ptr(split),
             _lib.ptr(counts), _lib.stream()), "pc_densify_masks")
-        n_keep, n_split = (int(v) for v in counts.cpu().tolist())
-        if n_keep == 0:
-            raise RuntimeError("all balls pruned; lower the densify p0_min")
-        if max_balls is not None and n_keep + n_split > max_balls:
-            allowed = max(0, int(max_balls) - n_keep)
-            split = (split.bool() & (torch.cumsum(split.to(torch.int64), 0)
-                                     <= allowed)).to(torch.uint8)
-            n_split = allowed if allowed < n_split else n_split
         ws = torch.empty(int(lib.pc_compact_workspace_bytes(B)),
                          dtype=torch.uint8, device=dev)
         index = torch.empty(2 * B, dtype=torch.int64, device=dev)
@@ -688,6 +734,11 @@ class IterationEngine:
             _lib.ptr(keep), _lib.ptr(split), B, _lib.ptr(index),
             _lib.ptr(n_out), _lib.ptr(ws), ws.numel(), _lib.stream()),
             "pc_compact_index")
+        n_keep, n_split = (int(v) for v in counts.cpu().tolist())   # the sync
+        if n_keep == 0:
+            raise RuntimeError("all balls pruned; lower the densify p0_min")
+        if max_balls is not None:
+            n_split = min(n_split, max(0, int(max_balls) - n_keep))
         B2 = n_keep + n_split
         index = index[:B2]
         per_channel = self.basis == "gauss" and self.params["theta"].dim() == 3
@@ -708,9 +759,11 @@ class IterationEngine:
                    new.offset + new.size].zero_()
                 V2[new.offset + (new.size // B2) * n_keep:
                    new.offset + new.size].zero_()
-        halve = torch.index_select(split, 0, index)
-        child = torch.zeros(B2, dtype=torch.uint8, device=dev)
-        child[n_keep:] = 1
+        halve = torch.empty(B2, dtype=torch.uint8, device=dev)
+        child = torch.empty(B2, dtype=torch.uint8, device=dev)
+        _lib.check(lib.pc_densify_flags(
+            _lib.ptr(index), B, n_keep, B2, _lib.ptr(keep), _lib.ptr(halve),
+            _lib.ptr(child), _lib.stream()), "pc_densify_flags")
         pv = layout.views(P2)
         _lib.check(lib.pc_densify_apply(
             _lib.ptr(pv["p0"]), _lib.ptr(pv["mu"]), _lib.ptr(pv["a0"]),

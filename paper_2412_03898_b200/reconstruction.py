@@ -221,15 +221,19 @@ def dynamic_reconstruct(observed, array, init_balls, config, roi=None,
     cloud = identity_cloud(p0, a0, mu, nb, basis)
     eng = IterationEngine(cloud, array, observed_frame_major(observed),
                           observed.frame_times, config)
+    eng.stage_timing = progress is not None
     rng = np.random.default_rng(config.seed)
     for it in range(config.dynamic_iters):
         frames = select_frames(observed.n_frames, config.frame_batch, rng)
         loss = eng.iterate(it, frames)
         if progress is not None:
+            # the reference's record (reconstruction.py:329-332) plus the
+            # device stage timings of this iteration (CUDA events)
             progress({"stage": "dynamic", "iteration": it, "loss": loss,
                       "n_balls": eng.B,
                       "frames": [int(k) for k in frames],
-                      **{f"lr_{k}": v for k, v in eng.last_lrs.items()}})
+                      **{f"lr_{k}": v for k, v in eng.last_lrs.items()},
+                      **(eng.last_timing or {})})
     out = eng.cloud()
     if roi is not None:
         _warn_outside_roi(out, roi, observed.frame_times, config)

@@ -28,7 +28,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .core import DynamicCloud, ReconConfig, SensorArray, frame_times
+from .core import (DynamicCloud, ReconConfig, SensorArray,
+                   default_basis_grid, frame_times)
 
 GOLDEN_RATIO = (1.0 + np.sqrt(5.0)) / 2.0
 
@@ -177,7 +178,8 @@ def _motion(rng, mu, a0, axes, F, amp=0.08, period=8.0, drift=0.5):
 
 def make_problem(cfg_id: int, seed: int | None = None, scale: float = 1.0,
                  n_balls: int | None = None, n_sensors: int | None = None,
-                 n_frames: int | None = None, n_samples: int | None = None
+                 n_frames: int | None = None, n_samples: int | None = None,
+                 basis: str = "polyfourier", n_basis: int | None = None
                  ) -> Problem:
     """Build BASELINE config `cfg_id` (1-5); sizes may be overridden (tests
     use reduced instances with the same distributions)."""
@@ -225,9 +227,20 @@ def make_problem(cfg_id: int, seed: int | None = None, scale: float = 1.0,
     pos = q32(hemisphere(M, radius))
     array = SensorArray(pos, 1.5, 40.0, T, 0.0)
     gt = [(a_, p0, m_) for a_, _, m_ in _motion(rng, mu, a0, axes, F)]
-    omega = q32(rng.uniform(-0.01, 0.01, (B, 5, 8)))
-    cloud = DynamicCloud(p0, a0, mu, None, None, omega, basis="polyfourier")
-    cfg = ReconConfig(basis="polyfourier", n_basis=8)
+    if basis == "gauss":
+        # the reference's own default model: Gaussian basis on the default
+        # grid (core.py:152-163, n_basis 65 by default, core.py:468)
+        nb = 65 if n_basis is None else int(n_basis)
+        th, sg = default_basis_grid(nb)
+        omega = q32(rng.uniform(-0.01, 0.01, (B, 5, nb)))
+        cloud = DynamicCloud(p0, a0, mu, np.tile(th, (B, 1)),
+                             np.tile(sg, (B, 1)), omega)
+        cfg = ReconConfig(n_basis=nb)
+    else:
+        omega = q32(rng.uniform(-0.01, 0.01, (B, 5, 8)))
+        cloud = DynamicCloud(p0, a0, mu, None, None, omega,
+                             basis="polyfourier")
+        cfg = ReconConfig(basis="polyfourier", n_basis=8)
     return Problem(f"config{cfg_id}", array, frame_times(F), gt, cloud, cfg,
                    {"shape": shp, "seed": seed, "half": half,
                     "radius": radius})

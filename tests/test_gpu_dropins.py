@@ -72,9 +72,9 @@ def _spherical_mean(R, t, p0, a0, v, n=4000):
     (the reference suite's oracle for the closed form, restated):
     p(R,t) = d/dt [t * mean over the sphere |x - R| = vt of p_init]."""
     def mean_times_t(tt):
-        r = v * tt
-        c = np.linspace(-1.0, 1.0, n)
-        d2 = R * R + r * r - 2 * R * r * c[None, :]
+        r = v * np.asarray(tt, dtype=np.float64)[:, None]
+        c = np.linspace(-1.0, 1.0, n)[None, :]
+        d2 = R * R + r * r - 2 * R * r * c
         f = p0 * np.exp(-d2 / (2 * a0 * a0))
         return tt * np.trapezoid(f, c, axis=1) / 2.0
     h = 1e-4
@@ -292,7 +292,7 @@ def test_cloud_states_at_float64_identity(pc):
 
 def test_cloud_states_at_floor_semantics(pc):
     """deformation.py:202-203: the floor applies whenever it is not None,
-    including a0_floor <= 0 (here -1 does nothing, 0.5 clamps)."""
+    including a0_floor <= 0."""
     from paper_2412_03898_b200.core import default_basis_grid
     B, N = 4, 3
     th, sg = default_basis_grid(N)
@@ -301,12 +301,13 @@ def test_cloud_states_at_floor_semantics(pc):
     cloud = pc.DynamicCloud(np.ones(B), np.ones(B), np.ones((B, 3)),
                             np.tile(th, (B, 1)), np.tile(sg, (B, 1)), om)
     ref_none = oracle.cloud_states_at(cloud, 0.5)
-    got = pc.cloud_states_at(cloud, 0.5, a0_floor=-1.0)
+    assert np.all(ref_none.a0_t < -1.4)            # a0 (1 + H0) < 0 here
+    got = pc.cloud_states_at(cloud, 0.5)           # no floor: unclamped
     assert np.allclose(got.a0_t, ref_none.a0_t, rtol=1e-14)
-    got = pc.cloud_states_at(cloud, 0.5, a0_floor=0.5)
-    assert np.all(got.a0_t == 0.5)
-    got = pc.cloud_states_at(cloud, 0.5, a0_floor=0.0)
-    assert np.allclose(got.a0_t, np.maximum(ref_none.a0_t, 0.0), rtol=1e-14)
+    for floor in (-2.0, -1.0, 0.0, 0.5):
+        got = pc.cloud_states_at(cloud, 0.5, a0_floor=floor)
+        assert np.allclose(got.a0_t, np.maximum(ref_none.a0_t, floor),
+                           rtol=1e-14), floor
 
 
 # ------------------------------------------------ optimiser drop-ins (A8)

@@ -286,6 +286,9 @@ def test_dynamic_reconstruct_golden(pc, golden):
     cloud = pc.dynamic_reconstruct(obs, arr, init, cfg, progress=log.append)
     losses = [r["loss"] for r in log]
     assert rel_l2(losses, g["dyn_loss"]) < SIGNAL_TOL
+    # progress records carry the device stage timings (CUDA events)
+    assert all(r["grads_ms"] > 0 and r["iteration_ms"] >= r["grads_ms"]
+               and r["pair_evals_per_s"] > 0 for r in log)
     for nm in ("p0", "a0", "mu", "theta", "sigma", "omega"):
         ref = g["dyn_out_" + nm]
         got = getattr(cloud, nm)
@@ -484,15 +487,50 @@ def _engine_small(pc, B=3000, seed=4, spatial=False):
     return prob, eng
 
 
-@pytest.mark.parametrize("B", [1000, 3000, 4097])
-def test_densify_threshold_is_numpy_percentile(pc, B):
+@pytest.mark.parametrize("B", [8, 9, 1000, 3000, 4097])
+@pytest.mark.parametrize("kind", ["normal", "ties", "tiny"])
+def test_densify_threshold_is_numpy_percentile(pc, B, kind):
+    """pc_abs_quantile_f32 (device radix select + numpy's _lerp) equals
+    numpy.percentile(|g|, q, 'linear') bit for bit: distinct values, heavy
+    ties (x_(k+1) = x_(k)), subnormal / zero magnitudes, several q."""
     import torch
     _, eng = _engine_small(pc, B)
     rng = np.random.default_rng(B)
-    g = rng.normal(size=B).astype(np.float32)
+    n = eng.B
+    g = rng.normal(size=n).astype(np.float32)
+    if kind == "ties":
+        g = np.round(g * 3).astype(np.float32) / 3
+    elif kind == "tiny":
+        g = (g * np.float32(1e-39)).astype(np.float32)
+        g[::7] = 0.0
     eng.grads["p0"].copy_(torch.as_tensor(g))
-    want = float(np.percentile(np.abs(g.astype(np.float64)), 90))
-    assert eng.p0_grad_threshold(90.0) == want
+    for q in (0.0, 37.5, 90.0, 99.9, 100.0):
+        want = float(np.percentile(np.abs(g.astype(np.float64)), q))
+        assert eng.p0_grad_threshold(q) == want, q
+
+
+def test_densify_cap_bit_exact(pc):
+    """max_balls truncates the children in parent order; parents whose child
+    was dropped keep their pressure (oracle.densify_plan(max_balls=...))."""
+    import torch
+    prob, eng = _engine_small(pc, 3000)
+    rng = np.random.default_rng(19)
+    B = eng.B
+    p0 = rng.uniform(0.0, 0.05, B)
+    g = rng.normal(size=B).astype(np.float32)
+    eng.params["p0"].copy_(torch.as_tensor(p0))
+    eng.grads["p0"].copy_(torch.as_tensor(g))
+    before = {k: v.cpu().numpy().copy() for k, v in eng.params.items()}
+    keep0 = ~(p0 < 0.01)
+    cap = int(keep0.sum()) + 57
+    n_pruned, n_children = eng.densify(p0_min=0.01, q=90.0, max_balls=cap)
+    keep, split, index, is_child = oracle.densify_plan(
+        p0, g.astype(np.float64), p0_min=0.01, q=90.0, max_balls=cap)
+    assert n_children == 57 == int(split.sum()) and eng.B == cap
+    want = oracle.apply_densify(before, index, is_child, split, keep)
+    got = eng.cloud()
+    for k in ("p0", "a0", "mu", "omega"):
+        assert np.array_equal(getattr(got, k), want[k]), k
 
 
 def test_densify_masks_order_and_params_bit_exact(pc):
