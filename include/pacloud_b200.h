@@ -363,8 +363,9 @@ int pc_densify_flags(const int64_t *index, int64_t n_balls, int64_t n_keep,
                      uint8_t *child, pc_stream_t stream);
 
 /* After the gather of a densify step (new order = survivors then children):
- * p0[i] *= 0.5 where halve[i] (split parents and their children) and
- * mu[i,0] += shift * a0[i] where child[i]. */
+ * p0[i] *= 0.5 where halve[i] (split parents and their children; halve may
+ * be NULL: the clone rule keeps p0) and mu[i,0] += shift * a0[i] where
+ * child[i]. */
 int pc_densify_apply(double *p0, double *mu, const double *a0,
                      const uint8_t *halve, const uint8_t *child,
                      int64_t n_balls, double shift, pc_stream_t stream);

@@ -488,14 +488,16 @@ def densify_plan(p0, gp0, p0_min=0.01, q=90.0, max_balls=None):
 
 
 def apply_densify(params: dict, index, is_child, split, keep,
-                  child_shift=0.5):
-    """Gather survivors + children; halve p0 of split parents and children;
-    shift each child's centre by +child_shift*a0 along x (builder-defined).
+                  child_shift=0.5, halve_pressure=False):
+    """Gather survivors + children (clones of their parents); with
+    `halve_pressure` halve p0 of split parents and children; shift each
+    child's centre by +child_shift*a0 along x (builder-defined).
     `params` maps name -> (B, ...) array; Adam moments are gathered with the
     same index and zeroed for children by the caller."""
     out = {k: np.array(v[index]) for k, v in params.items()}
-    halve = split[index]
-    out["p0"] = np.where(halve, 0.5 * out["p0"], out["p0"])
+    if halve_pressure:
+        halve = split[index]
+        out["p0"] = np.where(halve, 0.5 * out["p0"], out["p0"])
     if "mu" in out:
         shift = np.where(is_child, child_shift * out["a0"], 0.0)
         out["mu"][:, 0] = out["mu"][:, 0] + shift

@@ -59,7 +59,10 @@ namespace pc {
 #endif
 constexpr int FR_RUN = PC_FR_RUN;          // samples per run (register accumulators)
 constexpr int FR_CHUNK = PC_FR_CHUNK;      // balls per setup chunk
-constexpr int FR_WARPS = 8;
+#ifndef PC_FR_WARPS
+#define PC_FR_WARPS 8
+#endif
+constexpr int FR_WARPS = PC_FR_WARPS;
 constexpr int FR_THREADS = FR_WARPS * 32;
 constexpr int FR_GROUPS = FR_CHUNK / 32;
 constexpr int FR_QLEN = 64;                // per-warp ball queue (circular)

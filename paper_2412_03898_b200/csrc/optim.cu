@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256) k_densify_apply(double* __restrict__ p0,
                                                        int64_t n, double shift) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        if (halve[i]) p0[i] = 0.5 * p0[i];
+        if (halve && halve[i]) p0[i] = 0.5 * p0[i];
         if (child[i]) mu[3 * i] = mu[3 * i] + shift * a0[i];
     }
 }
@@ -513,7 +513,7 @@ extern "C" int pc_densify_apply(double* p0, double* mu, const double* a0, const 
                                 pc_stream_t stream) {
     if (n_balls < 0) return PC_ERR_ARGUMENT;
     if (n_balls == 0) return PC_OK;
-    if (!p0 || !mu || !a0 || !halve || !child) return PC_ERR_ARGUMENT;
+    if (!p0 || !mu || !a0 || !child) return PC_ERR_ARGUMENT;
     int64_t blocks = (n_balls + 255) / 256;
     if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
     k_densify_apply<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(p0, mu, a0, halve, child,

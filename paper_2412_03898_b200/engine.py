@@ -27,6 +27,7 @@ rank, i.e. broadcast).  Both end in the same gradient all-reduce.
 
 from __future__ import annotations
 
+import gc
 import math
 import os
 from dataclasses import dataclass
@@ -398,18 +399,27 @@ class IterationEngine:
         engine's own memory pool.  CUDAGraph.capture_begin/capture_end
         directly: the torch.cuda.graph context manager also runs
         gc.collect() and torch.cuda.empty_cache() before every capture,
-        which stalled the re-capture after a densify step for up to 1 s."""
+        which stalled the re-capture after a densify step for up to 1 s.
+        The cyclic garbage collector is paused for the capture instead: a
+        collection inside it could destroy another engine's CUDAGraph, and
+        cudaGraphExecDestroy during a global-mode capture invalidates it."""
         if self._pool is None:
             self._pool = torch.cuda.graph_pool_handle()
         g = torch.cuda.CUDAGraph()
         st = torch.cuda.Stream(device=self.device)
         st.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(st):
-            g.capture_begin(pool=self._pool)
-            try:
-                launch()
-            finally:
-                g.capture_end()
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.stream(st):
+                g.capture_begin(pool=self._pool)
+                try:
+                    launch()
+                finally:
+                    g.capture_end()
+        finally:
+            if gc_on:
+                gc.enable()
         torch.cuda.current_stream().wait_stream(st)
         return g
 
@@ -703,16 +713,19 @@ class IterationEngine:
         return float(self._p0_grad_threshold_dev(q).item())
 
     def densify(self, p0_min: float = 0.01, q: float = 90.0,
-                child_shift: float = 0.5, max_balls: int | None = None):
+                child_shift: float = 0.5, max_balls: int | None = None,
+                halve_pressure: bool = False):
         """Config-5 adaptive step (builder-defined): prune
         p0 < p0_min, split balls with |dL/dp0| above its q-th percentile.
         New order = survivors in order, then one child per split survivor in
         parent order (pc_compact_index), truncated to `max_balls`; every
         parameter and Adam moment is gathered (pc_gather_rows, step counts
-        preserved as in reconstruction.py:95-100); split parents and
-        children get half the pressure and children move +child_shift*a0
-        along x (pc_densify_flags + pc_densify_apply); children start with
-        zero moments.  Everything runs on the device; the one host read is
+        preserved as in reconstruction.py:95-100); a child is a clone of its
+        parent moved +child_shift*a0 along x (pc_densify_flags +
+        pc_densify_apply) and starts with zero moments.  `halve_pressure`
+        also halves the pressure of split parents and children (measured:
+        with it, repeated splits drive p0 under the absolute prune floor and
+        config 5 stalls near 125k balls instead of growing to 500k).  Everything runs on the device; the one host read is
         the (#keep, #split) pair that sizes the new cloud.
         Returns (n_pruned, n_children)."""
         lib = _lib.load_library()
@@ -767,7 +780,8 @@ class IterationEngine:
         pv = layout.views(P2)
         _lib.check(lib.pc_densify_apply(
             _lib.ptr(pv["p0"]), _lib.ptr(pv["mu"]), _lib.ptr(pv["a0"]),
-            _lib.ptr(halve), _lib.ptr(child), B2, float(child_shift),
+            _lib.ptr(halve) if halve_pressure else None, _lib.ptr(child), B2,
+            float(child_shift),
             _lib.stream()), "pc_densify_apply")
         # swap in the new cloud (internal order becomes the caller's order)
         self.layout, self.B = layout, B2

@@ -533,7 +533,8 @@ def test_densify_cap_bit_exact(pc):
         assert np.array_equal(getattr(got, k), want[k]), k
 
 
-def test_densify_masks_order_and_params_bit_exact(pc):
+@pytest.mark.parametrize("halve", [False, True])
+def test_densify_masks_order_and_params_bit_exact(pc, halve):
     import torch
     prob, eng = _engine_small(pc, 2000)
     rng = np.random.default_rng(9)
@@ -543,12 +544,13 @@ def test_densify_masks_order_and_params_bit_exact(pc):
     eng.params["p0"].copy_(torch.as_tensor(p0))
     eng.grads["p0"].copy_(torch.as_tensor(g))
     before = {k: v.cpu().numpy().copy() for k, v in eng.params.items()}
-    n_pruned, n_children = eng.densify(p0_min=0.01, q=90.0, child_shift=0.5)
+    n_pruned, n_children = eng.densify(p0_min=0.01, q=90.0, child_shift=0.5,
+                                       halve_pressure=halve)
     keep, split, index, is_child = oracle.densify_plan(
         p0, g.astype(np.float64), p0_min=0.01, q=90.0)
     assert n_pruned == int((~keep).sum()) and n_children == int(split.sum())
     want = oracle.apply_densify(before, index, is_child, split, keep,
-                                child_shift=0.5)
+                                child_shift=0.5, halve_pressure=halve)
     got = eng.cloud()
     for k in ("p0", "a0", "mu", "omega"):
         assert np.array_equal(getattr(got, k), want[k]), k

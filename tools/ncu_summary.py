@@ -1,6 +1,6 @@
 """Summarise ncu captures for profiles/ (run in the build container).
 
-    python tools/ncu_summary.py full  <report.ncu-rep> <out.json>
+    python tools/ncu_summary.py full  <report.ncu-rep | raw.csv> <out.json>
     python tools/ncu_summary.py launches <launches.csv> <out.json>
 
 `full`: per kernel the time, pipe utilisations, issue efficiency, DRAM
@@ -48,8 +48,11 @@ SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0,
 
 
 def full(rep, out):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
-                         capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):          # `ncu -i X --page raw --csv` exported on the box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
     res = []
