@@ -12,10 +12,12 @@
 //           (R, window [jl, jh), wavefront offset X at the reference sample
 //           jr) into a 16-byte record + the window word; per 32-ball group
 //           the span of runs its windows touch.
-//   runs    one warp per run at a time (dynamic): the warp scans the groups
-//           whose span holds the run, compacts the balls whose window meets
-//           the run into a per-warp queue (ball order kept), and processes
-//           the queue 32 balls at a time, ONE BALL PER LANE: each lane sweeps
+//   runs    one warp per run at a time (dynamic, index order): the warp
+//           scans the groups whose span holds the run; a group whose 32
+//           balls all meet the run is swept directly (lane = ball), the
+//           others' overlapping balls are compacted into a per-warp queue
+//           (ball order kept) that is swept 32 balls at a time, ONE BALL PER
+//           LANE: each lane sweeps
 //           all RUN samples of its ball with the Gaussian-on-grid recurrence
 //           (e <- e g, g <- g h over two packed f32x2 chains, re-seeded by
 //           MUFU every 16 samples) into RUN accumulators held in REGISTERS.
@@ -50,6 +52,23 @@ namespace pc {
 #endif
 #ifndef PC_FR_CHUNK
 #define PC_FR_CHUNK 1024
+#endif
+#ifndef PC_FR_DIRECT
+#define PC_FR_DIRECT 1
+#endif
+#ifndef PC_FR_CHAIN1
+#define PC_FR_CHAIN1 0
+#endif
+// PC_FR_ORDER 1: warp 0 orders each chunk's runs by weight (longest first)
+// between the chunk's barriers; 0 (default): runs taken in index order, no
+// run-weight bookkeeping (config 3 forward, same box: 303.3 vs 309.7 ms).
+// PC_FR_DIRECT 1 (default): a group whose 32 balls all meet the run is swept
+// directly, lane = ball, without the queue round trip (with ORDER 0:
+// 280.4 vs 303.3 ms).  PC_FR_CHAIN1 1: one recurrence chain per ball-run (4
+// MUFU seeds instead of 8; 284.2 with ORDER 0 + DIRECT, parity 1.3e-6 vs
+// 4.2e-7): off.
+#ifndef PC_FR_ORDER
+#define PC_FR_ORDER 0
 #endif
 #ifndef PC_FR_LPT
 #define PC_FR_LPT 1
@@ -117,6 +136,30 @@ static size_t fr_smem_bytes(int T) {
 // balls are bit-exact).
 __device__ __forceinline__ void fr_fast(float2 (&acc)[FR_RUN / 2], float x0, float vs, float cs) {
     static_assert(FR_RUN == 32, "two interleaved 16-sample halves");
+#if PC_FR_CHAIN1
+    // one packed chain over the whole run: 4 MUFU seeds instead of 8 (the
+    // seed may sit up to 31 samples before the window: fr_vs_max)
+    {
+        const float D = 2.f * vs;
+        const float2 mcD = splat2(-cs * D);
+        const float2 h2 = splat2(ex2(-2.f * D * D));
+        const float2 xa = make_float2(x0, x0 - vs);
+        const float2 xxa = fmul2(xa, xa);
+        float2 ea = make_float2(ex2(FR_SCALE_EXP - xxa.x), ex2(FR_SCALE_EXP - xxa.y));
+        float2 ga = ex2_2(ffma2(xa, splat2(2.f * D), splat2(-D * D)));
+        float2 ca = fmul2(splat2(cs), xa);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            acc[k] = ffma2(ca, ea, acc[k]);
+            if (k < 15) {
+                ea = fmul2(ea, ga);
+                ga = fmul2(ga, h2);
+                ca = fadd2(ca, mcD);
+            }
+        }
+        return;
+    }
+#endif
     const float D = 2.f * vs;
     const float2 mcD = splat2(-cs * D);
     const float2 h2 = splat2(ex2(-2.f * D * D));
@@ -272,10 +315,12 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                 if (q1 >= q0) {
                     atomicMin(cc + 1, q0);
                     atomicMax(cc + 2, q1);
+#if PC_FR_ORDER
                     // run weight (groups whose span holds the run, the task
                     // order's work proxy) as a difference array
                     atomicAdd(runw + q0, 1);
                     atomicAdd(runw + q1 + 1, -1);
+#endif
                 }
             }
         }
@@ -292,7 +337,7 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
         // warp 0: runs by descending weight (counting sort on min(w, 31)), so
         // the long runs start first and the chunk ends on short ones (the
         // order does not change any result: each run is summed by one warp)
-        if (warp == 0 && nrun > 0) {
+        if (PC_FR_ORDER && warp == 0 && nrun > 0) {
             // weights: inclusive prefix of the difference array (runs 0..rhi;
             // runs below rlo hold 0), the array zeroed for the next chunk
             int carry = 0;
@@ -336,12 +381,12 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             if (lane == 0) k = atomicAdd(cc, 1);
             k = __shfl_sync(0xffffffffu, k, 0);
             if (k >= nrun) break;
-            const int q = PC_FR_LPT ? rorder[k] : rlo + k;
+            const int q = (PC_FR_ORDER && PC_FR_LPT) ? rorder[k] : rlo + k;
             const int j0 = q * FR_RUN;
             float2 acc[FR_RUN / 2];
 #pragma unroll
             for (int k = 0; k < FR_RUN / 2; ++k) acc[k] = splat2(0.f);
-            int qn = 0, qd = 0;
+            int qn = 0, qd = 0, nd = 0;   // nd: a full group went the direct way
             for (int gb = 0; gb < FR_GROUPS; gb += 32) {
                 const unsigned sp = gspan[gb + lane];
                 const bool gh = (int)(sp & 0xffff) <= q && q <= (int)(sp >> 16);
@@ -353,6 +398,22 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                     const unsigned wb = recB[i];
                     const unsigned hm = __ballot_sync(0xffffffffu, (int)(wb & 0xffff) < j0 + FR_RUN &&
                                                                        (int)(wb >> 16) > j0);
+#if PC_FR_DIRECT
+                if (hm == 0xffffffffu) {
+                    // the whole group meets the run: each lane takes its own
+                    // ball directly (no queue round trip)
+                    const float4 r = recA[i];
+                    const int w = __float_as_int(r.w);
+                    if (!(w & (1 << 30))) {
+                        fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                    } else {
+                        fr_slow(acc, j0, r.x, recY[i], r.z, r.y, w & 0xffff, wb & 0xffff,
+                                wb >> 16, w < 0);
+                    }
+                    nd = 1;
+                    continue;
+                }
+#endif
                     if ((hm >> lane) & 1u) Q[(qn + __popc(hm & lt)) & (FR_QLEN - 1)] = (unsigned short)i;
                     qn += __popc(hm);
                     if (qn - qd >= 32) {
@@ -384,7 +445,7 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                             w < 0);
                 }
             }
-            if (qn == 0) continue;
+            if (qn == 0 && nd == 0) continue;
             // ---- sum the 32 lanes' partial runs per sample, in lane order:
             // 16 samples at a time through a [32][XPAD] transpose
 #pragma unroll
@@ -490,7 +551,7 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
 // stay a normal float: x^2 <= 196 (margin to 206)
 static float fr_vs_max(double support) {
     const double xe = 0.8493218002880191 * support;
-    const double v = (14.0 - xe) / 17.0;
+    const double v = (14.0 - xe) / (PC_FR_CHAIN1 ? 33.0 : 17.0);
     return v > 0 ? (float)v : 0.f;
 }
 
