@@ -43,6 +43,8 @@
 // direct path (MUFU per sample, exact window clip [jl, jh) as the reference).
 // Samples the fast path adds outside a pair's +-6 sigma window weigh
 // < e^-18 of its peak (the reference's fast path drops them).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace pc {
@@ -55,6 +57,9 @@ namespace pc {
 #endif
 #ifndef PC_FR_DIRECT
 #define PC_FR_DIRECT 1
+#endif
+#ifndef PC_FR_DIRECT_MIN
+#define PC_FR_DIRECT_MIN 32
 #endif
 #ifndef PC_FR_CHAIN1
 #define PC_FR_CHAIN1 0
@@ -73,8 +78,11 @@ namespace pc {
 #ifndef PC_FR_LPT
 #define PC_FR_LPT 1
 #endif
+// 4 CTAs (32 warps) per SM: 64 registers (small spill) and the 9 KB
+// transpose buffer (PC_FR_XQ 1) keep the CTA under 57 KB of shared memory
+// (config 3 forward 273.1 ms vs 279.9 at 3 CTAs / 80 registers / 20 KB)
 #ifndef PC_FR_MINB
-#define PC_FR_MINB 3
+#define PC_FR_MINB 4
 #endif
 constexpr int FR_RUN = PC_FR_RUN;          // samples per run (register accumulators)
 constexpr int FR_CHUNK = PC_FR_CHUNK;      // balls per setup chunk
@@ -85,7 +93,14 @@ constexpr int FR_WARPS = PC_FR_WARPS;
 constexpr int FR_THREADS = FR_WARPS * 32;
 constexpr int FR_GROUPS = FR_CHUNK / 32;
 constexpr int FR_QLEN = 64;                // per-warp ball queue (circular)
-constexpr int FR_XPAD = 20;                // transpose row stride (16 + 4 floats)
+// Transpose of the 32 lanes' partial runs: PC_FR_XQ 0: 16 samples at a time
+// through [32][20] float rows (float4 stores); 1: 8 samples at a time
+// through [32][9] rows (scalar stores, conflict-free), 9 KB instead of 20 KB
+// of shared memory per CTA.
+#ifndef PC_FR_XQ
+#define PC_FR_XQ 1
+#endif
+constexpr int FR_XPAD = PC_FR_XQ ? 9 : 20;  // transpose row stride (floats)
 constexpr float FR_SCALE_EXP = 80.f;       // chains carry c 2^(80 - x^2)
 
 struct FwdRunArgs {
@@ -211,6 +226,139 @@ __device__ __forceinline__ void fr_slow(float2 (&acc)[FR_RUN / 2], int j0, float
         const float sc = cs * 1.2089258196146292e24f;   // 2^80
         if (j >= jl && j < jh) acc[k].x = fmaf(sc, v.x, acc[k].x);
         if (j + 1 >= jl && j + 1 < jh) acc[k].y = fmaf(sc, v.y, acc[k].y);
+    }
+}
+
+// Sum the 32 lanes' partial runs per sample in a fixed order and add the
+// run to the row (scaled back by 2^-80).
+__device__ __forceinline__ void fr_flush(const float2 (&acc)[FR_RUN / 2], float* xb, float* trace,
+                                         int j0, int Tp) {
+    const int lane = threadIdx.x & 31;
+#if PC_FR_XQ
+#pragma unroll
+    for (int qq = 0; qq < FR_RUN / 8; ++qq) {
+        __syncwarp();
+        float* rowp = xb + lane * FR_XPAD;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            rowp[2 * u] = acc[4 * qq + u].x;
+            rowp[2 * u + 1] = acc[4 * qq + u].y;
+        }
+        __syncwarp();
+        // lane = column c (8) x row block p (4 blocks of 8 rows)
+        const int col = lane & 7, r0 = (lane >> 3) * 8;
+        float sacc = 0.f;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) sacc += xb[(r0 + r) * FR_XPAD + col];
+        sacc += __shfl_down_sync(0xffffffffu, sacc, 16);
+        sacc += __shfl_down_sync(0xffffffffu, sacc, 8);
+        if (lane < 8) {
+            // chain a holds samples 0..15 (acc 0..7), chain b 16..31
+            const int j = j0 + 8 * qq + col;
+            if (j < Tp) trace[j] += sacc * 8.271806125530277e-25f;   // 2^-80
+        }
+    }
+#else
+#pragma unroll
+    for (int hb = 0; hb < FR_RUN / 16; ++hb) {
+        __syncwarp();
+        float4* rowp = reinterpret_cast<float4*>(xb + lane * FR_XPAD);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            rowp[k] = make_float4(acc[8 * hb + 2 * k].x, acc[8 * hb + 2 * k].y,
+                                  acc[8 * hb + 2 * k + 1].x, acc[8 * hb + 2 * k + 1].y);
+        __syncwarp();
+        // lane c < 16 sums rows 0..15 of column c, lane 16 + c rows 16..31
+        const int col = lane & 15, r0 = lane & 16;
+        float sacc = 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sacc += xb[(r0 + r) * FR_XPAD + col];
+        const float other = __shfl_down_sync(0xffffffffu, sacc, 16);
+        if (lane < 16) {
+            const int j = j0 + 16 * hb + col;
+            if (j < Tp) trace[j] += (sacc + other) * 8.271806125530277e-25f;   // 2^-80
+        }
+    }
+#endif
+}
+
+// Row epilogue shared by the forward kernels: relative tail threshold,
+// residual against the observed row, the row's fp64 L2 partial, one
+// (vectorised when aligned) store.
+__device__ __forceinline__ void fr_epilogue(const FwdRunArgs& a, const float* trace, float* xbuf,
+                                            int T, size_t row) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // Samples below 2^-60 of the row's peak are set to zero: the fast path
+    // sums the far Gaussian tails outside each pair's window (the reference
+    // drops them), where products leave fp32's normal range; a threshold
+    // RELATIVE to the row keeps the output exactly linear in p0.
+    float mx = 0.f;
+    for (int j = tid; j < T; j += FR_THREADS) mx = fmaxf(mx, fabsf(trace[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float* redf = reinterpret_cast<float*>(xbuf);
+    if (lane == 0) redf[warp] = mx;
+    __syncthreads();
+    mx = 0.f;
+#pragma unroll
+    for (int w = 0; w < FR_WARPS; ++w) mx = fmaxf(mx, redf[w]);
+    const float thr = mx * 8.673617379884035e-19f;    // 2^-60
+    const size_t base = row * (size_t)T;
+    double lsum = 0.0;
+    const bool vec = (T & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.out) |
+                                       reinterpret_cast<uintptr_t>(a.obs)) & 15) == 0;
+    if (vec) {
+        const int T4 = T >> 2;
+        float4* o4 = reinterpret_cast<float4*>(a.out + base);
+        const float4* t4 = reinterpret_cast<const float4*>(trace);
+        if (a.obs) {
+            const float4* b4 = reinterpret_cast<const float4*>(a.obs + base);
+            for (int j = tid; j < T4; j += FR_THREADS) {
+                float4 p = t4[j];
+                const float4 ob = __ldcs(b4 + j);
+                p.x = fabsf(p.x) < thr ? 0.f : p.x;
+                p.y = fabsf(p.y) < thr ? 0.f : p.y;
+                p.z = fabsf(p.z) < thr ? 0.f : p.z;
+                p.w = fabsf(p.w) < thr ? 0.f : p.w;
+                const float4 r = make_float4(p.x - ob.x, p.y - ob.y, p.z - ob.z, p.w - ob.w);
+                lsum = fma((double)r.x, (double)r.x, lsum);
+                lsum = fma((double)r.y, (double)r.y, lsum);
+                lsum = fma((double)r.z, (double)r.z, lsum);
+                lsum = fma((double)r.w, (double)r.w, lsum);
+                o4[j] = r;
+            }
+        } else {
+            for (int j = tid; j < T4; j += FR_THREADS) {
+                float4 p = t4[j];
+                p.x = fabsf(p.x) < thr ? 0.f : p.x;
+                p.y = fabsf(p.y) < thr ? 0.f : p.y;
+                p.z = fabsf(p.z) < thr ? 0.f : p.z;
+                p.w = fabsf(p.w) < thr ? 0.f : p.w;
+                o4[j] = p;
+            }
+        }
+    } else {
+        for (int j = tid; j < T; j += FR_THREADS) {
+            float r = trace[j];
+            r = fabsf(r) < thr ? 0.f : r;
+            if (a.obs) {
+                r -= a.obs[base + j];
+                lsum = fma((double)r, (double)r, lsum);
+            }
+            a.out[base + j] = r;
+        }
+    }
+    if (a.loss) {
+        double* red = reinterpret_cast<double*>(xbuf);
+        __syncthreads();
+        lsum = warp_sum(lsum);
+        if (lane == 0) red[warp] = lsum;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < FR_WARPS; ++w) t += red[w];
+            a.loss[row] = t;
+        }
     }
 }
 
@@ -399,16 +547,19 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                     const unsigned hm = __ballot_sync(0xffffffffu, (int)(wb & 0xffff) < j0 + FR_RUN &&
                                                                        (int)(wb >> 16) > j0);
 #if PC_FR_DIRECT
-                if (hm == 0xffffffffu) {
-                    // the whole group meets the run: each lane takes its own
-                    // ball directly (no queue round trip)
-                    const float4 r = recA[i];
-                    const int w = __float_as_int(r.w);
-                    if (!(w & (1 << 30))) {
-                        fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
-                    } else {
-                        fr_slow(acc, j0, r.x, recY[i], r.z, r.y, w & 0xffff, wb & 0xffff,
-                                wb >> 16, w < 0);
+                if (__popc(hm) >= PC_FR_DIRECT_MIN) {
+                    // (nearly) the whole group meets the run: each lane takes
+                    // its own ball directly (no queue round trip); lanes whose
+                    // ball misses the run stay idle
+                    if ((hm >> lane) & 1u) {
+                        const float4 r = recA[i];
+                        const int w = __float_as_int(r.w);
+                        if (!(w & (1 << 30))) {
+                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                        } else {
+                            fr_slow(acc, j0, r.x, recY[i], r.z, r.y, w & 0xffff, wb & 0xffff,
+                                    wb >> 16, w < 0);
+                        }
                     }
                     nd = 1;
                     continue;
@@ -446,104 +597,12 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                 }
             }
             if (qn == 0 && nd == 0) continue;
-            // ---- sum the 32 lanes' partial runs per sample, in lane order:
-            // 16 samples at a time through a [32][XPAD] transpose
-#pragma unroll
-            for (int hb = 0; hb < FR_RUN / 16; ++hb) {
-                __syncwarp();
-                float4* rowp = reinterpret_cast<float4*>(xb + lane * FR_XPAD);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    rowp[k] = make_float4(acc[8 * hb + 2 * k].x, acc[8 * hb + 2 * k].y,
-                                          acc[8 * hb + 2 * k + 1].x, acc[8 * hb + 2 * k + 1].y);
-                __syncwarp();
-                // lane c < 16 sums rows 0..15 of column c, lane 16 + c rows 16..31
-                const int col = lane & 15, r0 = lane & 16;
-                float sacc = 0.f;
-#pragma unroll
-                for (int r = 0; r < 16; ++r) sacc += xb[(r0 + r) * FR_XPAD + col];
-                const float other = __shfl_down_sync(0xffffffffu, sacc, 16);
-                if (lane < 16) {
-                    const int j = j0 + 16 * hb + col;
-                    if (j < Tp) trace[j] += (sacc + other) * 8.271806125530277e-25f;   // 2^-80
-                }
-            }
+            // ---- sum the 32 lanes' partial runs per sample (fixed order)
+            fr_flush(acc, xb, trace, j0, Tp);
         }
         __syncthreads();
     }
-    // -------------------------------------------------------------- epilogue
-    // Samples below 2^-60 of the row's peak are set to zero: the fast path
-    // sums the far Gaussian tails outside each pair's window (the reference
-    // drops them), where products leave fp32's normal range; a threshold
-    // RELATIVE to the row keeps the output exactly linear in p0.
-    float mx = 0.f;
-    for (int j = tid; j < T; j += FR_THREADS) mx = fmaxf(mx, fabsf(trace[j]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float* redf = reinterpret_cast<float*>(xbuf);
-    if (lane == 0) redf[warp] = mx;
-    __syncthreads();
-    mx = 0.f;
-#pragma unroll
-    for (int w = 0; w < FR_WARPS; ++w) mx = fmaxf(mx, redf[w]);
-    const float thr = mx * 8.673617379884035e-19f;    // 2^-60
-    const size_t base = row * (size_t)T;
-    double lsum = 0.0;
-    const bool vec = (T & 3) == 0 && ((reinterpret_cast<uintptr_t>(a.out) |
-                                       reinterpret_cast<uintptr_t>(a.obs)) & 15) == 0;
-    if (vec) {
-        const int T4 = T >> 2;
-        float4* o4 = reinterpret_cast<float4*>(a.out + base);
-        const float4* t4 = reinterpret_cast<const float4*>(trace);
-        if (a.obs) {
-            const float4* b4 = reinterpret_cast<const float4*>(a.obs + base);
-            for (int j = tid; j < T4; j += FR_THREADS) {
-                float4 p = t4[j];
-                const float4 ob = __ldcs(b4 + j);
-                p.x = fabsf(p.x) < thr ? 0.f : p.x;
-                p.y = fabsf(p.y) < thr ? 0.f : p.y;
-                p.z = fabsf(p.z) < thr ? 0.f : p.z;
-                p.w = fabsf(p.w) < thr ? 0.f : p.w;
-                const float4 r = make_float4(p.x - ob.x, p.y - ob.y, p.z - ob.z, p.w - ob.w);
-                lsum = fma((double)r.x, (double)r.x, lsum);
-                lsum = fma((double)r.y, (double)r.y, lsum);
-                lsum = fma((double)r.z, (double)r.z, lsum);
-                lsum = fma((double)r.w, (double)r.w, lsum);
-                o4[j] = r;
-            }
-        } else {
-            for (int j = tid; j < T4; j += FR_THREADS) {
-                float4 p = t4[j];
-                p.x = fabsf(p.x) < thr ? 0.f : p.x;
-                p.y = fabsf(p.y) < thr ? 0.f : p.y;
-                p.z = fabsf(p.z) < thr ? 0.f : p.z;
-                p.w = fabsf(p.w) < thr ? 0.f : p.w;
-                o4[j] = p;
-            }
-        }
-    } else {
-        for (int j = tid; j < T; j += FR_THREADS) {
-            float r = trace[j];
-            r = fabsf(r) < thr ? 0.f : r;
-            if (a.obs) {
-                r -= a.obs[base + j];
-                lsum = fma((double)r, (double)r, lsum);
-            }
-            a.out[base + j] = r;
-        }
-    }
-    if (a.loss) {
-        double* red = reinterpret_cast<double*>(xbuf);
-        __syncthreads();
-        lsum = warp_sum(lsum);
-        if (lane == 0) red[warp] = lsum;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < FR_WARPS; ++w) t += red[w];
-            a.loss[row] = t;
-        }
-    }
+    fr_epilogue(a, trace, xbuf, T, row);
 }
 
 // recurrence bound: the seed x of a half run is at most the window edge

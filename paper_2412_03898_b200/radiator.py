@@ -104,6 +104,40 @@ class DeviceArray:
             int(n_balls), int(n_frames), ctypes.byref(self.struct)))
 
 
+_DARR_CACHE: "OrderedDict" = None
+
+
+def cached_device_array(array, support_sigmas=DEFAULT_SUPPORT_SIGMAS,
+                        exact=False) -> DeviceArray:
+    """DeviceArray of a host SensorArray, reused across the per-frame
+    drop-in calls (a patched reference loop calls forward_frame and
+    accumulate_frame_grads once per frame with the same array): keyed by
+    the array's scalars and a digest of its positions, 8 entries, LRU.
+    Device-tensor positions are not cached."""
+    global _DARR_CACHE
+    from collections import OrderedDict
+    import hashlib
+    pos = array.positions
+    if isinstance(pos, torch.Tensor):
+        return DeviceArray(array, support_sigmas, exact)
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    key = (hashlib.blake2b(pos.tobytes(), digest_size=16).digest(), pos.shape,
+           float(array.sound_speed), float(array.sample_rate),
+           int(array.n_samples), float(array.t_start), float(support_sigmas),
+           bool(exact), torch.cuda.current_device())
+    if _DARR_CACHE is None:
+        _DARR_CACHE = OrderedDict()
+    d = _DARR_CACHE.get(key)
+    if d is None:
+        d = DeviceArray(array, support_sigmas, exact)
+        _DARR_CACHE[key] = d
+        if len(_DARR_CACHE) > 8:
+            _DARR_CACHE.popitem(last=False)
+    else:
+        _DARR_CACHE.move_to_end(key)
+    return d
+
+
 def forward_device(darr: DeviceArray, mu_t, a0_t, p0_t, observed=None,
                    out=None, loss=None, coincident=None, workspace=None):
     """pc_forward_traces on device tensors.
@@ -307,7 +341,7 @@ def forward_frame(states, array, support_sigmas: float = DEFAULT_SUPPORT_SIGMAS,
     """Superpose every ball's pressure trace at every sensor -> (M, T)."""
     state = _as_cloud_state(states)
     torch_io = _is_torch(state.a0_t, state.mu_t)
-    darr = DeviceArray(array, support_sigmas, exact)
+    darr = cached_device_array(array, support_sigmas, exact)
     B = len(state)
     if B == 0:
         z = torch.zeros((darr.M, darr.T), dtype=torch.float64,
@@ -337,7 +371,7 @@ def frame_state_grads(states, array, residual,
     if B == 0:
         z = torch.zeros((0, 5), dtype=torch.float64, device=_device())
         return z if torch_io else z.cpu().numpy()
-    darr = DeviceArray(array, support_sigmas, exact)
+    darr = cached_device_array(array, support_sigmas, exact)
     mu, a0, p0 = _state_tensors(state)
     r = to_device(residual, torch.float32).reshape(1, M, T)
     G, coinc = state_grads_device(darr, mu, a0, p0, r)
@@ -366,7 +400,7 @@ def accumulate_frame_grads(states, state_grads, array, residual,
     if B == 0:
         G = torch.zeros((1, 0, 5), dtype=torch.float32, device=dev)
     else:
-        darr = DeviceArray(array, support_sigmas, exact)
+        darr = cached_device_array(array, support_sigmas, exact)
         mu, a0, p0 = _state_tensors(state)
         r = to_device(residual, torch.float32).reshape(1, M, T)
         G, coinc = state_grads_device(darr, mu, a0, p0, r)
