@@ -1175,323 +1175,6 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     }
 }
 
-// ---------------------------------------------------------------- adjoint,
-// two balls per warp (PC_ADJ2=1; measured slower, kept for A/B)
-//
-// The same sweep as k_adjoint, but a warp owns two Morton-adjacent balls
-// (CTA = 2 ADJ_WARPS balls): for each sensor the 2-lane group sweeps the
-// UNION of the two balls' windows once, and every residual quad it loads
-// feeds both balls' moment sums (four accum_pair_mufu per 16-byte load
-// instead of two).  Adjacent balls reach a sensor within a few samples of
-// each other, so the union is barely longer than either window, while the
-// L1 traffic and the load latency per sample-evaluation halve.  A pair of
-// windows that do not overlap well (2 union > len0 + len1 + ADJ2_SLACK),
-// the near-field / exact paths and lone balls fall back to k_adjoint's
-// one-ball sweep.  Samples a ball sweeps outside its own +-6 sigma window
-// weigh < 2^-26 of its peak (the reference's fast path drops them; the
-// one-ball sweep already adds up to 3 at each end).  Deterministic: fixed
-// per-lane order, one xor reduction per ball.
-//
-// Measured (B200, same box, adjoint ms): config 3 367.8 (k_adjoint) vs
-// 385.5 / 378.1 / 422.2 with slack 64 / 160 / 32, 457.8 / 446.4 at 80 / 64
-// registers (launch bounds 6 / 8 CTAs); config 2 4.89 vs 5.62 / 5.30.  The
-// kernel is pipe-bound (FMA 62 %, XU 66 %), not load-bound: sharing the
-// loads saves L1 traffic but the union windows add work and the 96
-// registers cut residency from 32 to 20 warps per SM.
-
-#ifndef PC_ADJ2
-#define PC_ADJ2 0
-#endif
-#ifndef PC_ADJ2_SLACK
-#define PC_ADJ2_SLACK 64
-#endif
-
-template <bool ALIGNED>
-__device__ __forceinline__ void adj_sweep_one(const float* __restrict__ row, int T, int sub,
-                                              float4 r0, int jh, bool fast, float vs, float D,
-                                              float Yr, float2& A0, float2& A1, float2& A2,
-                                              float2& A3) {
-    const int w = __float_as_int(r0.x);
-    const int jl = w & 0x3fffffff;
-    const bool near = (w >> 30) & 1;
-    const int je1 = (jh + 3) & ~3;
-    int j = (jl & ~3) + 4 * sub;
-    if (j >= je1) return;
-    const int jrr = __float_as_int(r0.y);
-    float2 k = make_float2((float)(j - jrr), (float)(j + 1 - jrr));
-    const float2 two = splat2(2.f);
-    const float2 mvs2 = splat2(-vs), vs2 = splat2(vs), mD2 = splat2(-D);
-    if (fast && !near) {
-        float2 xa = ffma2(k, mvs2, splat2(r0.z));
-        float2 xb = ffma2(fadd2(k, two), mvs2, splat2(r0.z));
-        int n = (je1 - j + LSTRIDE - 1) / LSTRIDE;
-        for (; n >= ADJ_CHUNK; n -= ADJ_CHUNK, j += ADJ_CHUNK * LSTRIDE) {
-            float4 rr[ADJ_CHUNK];
-#pragma unroll
-            for (int u = 0; u < ADJ_CHUNK; ++u) rr[u] = load_quad<ALIGNED>(row, j + u * LSTRIDE, T);
-#pragma unroll
-            for (int u = 0; u < ADJ_CHUNK; ++u) {
-                accum_pair_mufu(lo2(rr[u]), xa, A0, A1, A2, A3);
-                accum_pair_mufu(hi2(rr[u]), xb, A0, A1, A2, A3);
-                xa = fadd2(xa, mD2);
-                xb = fadd2(xb, mD2);
-            }
-        }
-        if (n > 0) {
-            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 q0 = load_quad<ALIGNED>(row, j, T);
-            const float4 q1 = n > 1 ? load_quad<ALIGNED>(row, j + LSTRIDE, T) : z;
-            const float4 q2 = n > 2 ? load_quad<ALIGNED>(row, j + 2 * LSTRIDE, T) : z;
-            accum_pair_mufu(lo2(q0), xa, A0, A1, A2, A3);
-            accum_pair_mufu(hi2(q0), xb, A0, A1, A2, A3);
-            if (n > 1) {
-                xa = fadd2(xa, mD2);
-                xb = fadd2(xb, mD2);
-                accum_pair_mufu(lo2(q1), xa, A0, A1, A2, A3);
-                accum_pair_mufu(hi2(q1), xb, A0, A1, A2, A3);
-            }
-            if (n > 2) {
-                xa = fadd2(xa, mD2);
-                xb = fadd2(xb, mD2);
-                accum_pair_mufu(lo2(q2), xa, A0, A1, A2, A3);
-                accum_pair_mufu(hi2(q2), xb, A0, A1, A2, A3);
-            }
-        }
-    } else {
-        const float2 kstep = splat2((float)LSTRIDE);
-        for (; j < je1; j += LSTRIDE) {
-            const float4 r = load_quad<ALIGNED>(row, j, T);
-            const float2 kb = fadd2(k, two);
-            const float2 xa = ffma2(k, mvs2, splat2(r0.z));
-            const float2 xb = ffma2(kb, mvs2, splat2(r0.z));
-            accum_pair(lo2(r), ex2n_2(fmul2(xa, xa)), xa, A0, A1, A2, A3);
-            accum_pair(hi2(r), ex2n_2(fmul2(xb, xb)), xb, A0, A1, A2, A3);
-            if (near) {
-                const float2 ya = ffma2(k, vs2, splat2(Yr));
-                const float2 yb = ffma2(kb, vs2, splat2(Yr));
-                accum_pair(lo2(r), ex2n_2(fmul2(ya, ya)), ya, A0, A1, A2, A3);
-                accum_pair(hi2(r), ex2n_2(fmul2(yb, yb)), yb, A0, A1, A2, A3);
-            }
-            k = fadd2(k, kstep);
-        }
-    }
-}
-
-// both balls over the union window [jl, jh) (fast far-field path only)
-template <bool ALIGNED>
-__device__ __forceinline__ void adj_sweep_two(const float* __restrict__ row, int T, int sub,
-                                              int jl, int jh, int jr0, float X0, float vs0,
-                                              int jr1, float X1, float vs1, float2& P0,
-                                              float2& P1, float2& P2, float2& P3, float2& Q0,
-                                              float2& Q1, float2& Q2, float2& Q3) {
-    const int je1 = (jh + 3) & ~3;
-    int j = (jl & ~3) + 4 * sub;
-    if (j >= je1) return;
-    const float2 two = splat2(2.f);
-    const float2 k0 = make_float2((float)(j - jr0), (float)(j + 1 - jr0));
-    const float2 k1 = make_float2((float)(j - jr1), (float)(j + 1 - jr1));
-    const float2 mv0 = splat2(-vs0), mv1 = splat2(-vs1);
-    const float2 mD0 = splat2(-(float)LSTRIDE * vs0), mD1 = splat2(-(float)LSTRIDE * vs1);
-    float2 xa = ffma2(k0, mv0, splat2(X0));
-    float2 xb = ffma2(fadd2(k0, two), mv0, splat2(X0));
-    float2 ya = ffma2(k1, mv1, splat2(X1));
-    float2 yb = ffma2(fadd2(k1, two), mv1, splat2(X1));
-#define PC_ADJ2_STEP(R)                                  \
-    accum_pair_mufu(lo2(R), xa, P0, P1, P2, P3);         \
-    accum_pair_mufu(hi2(R), xb, P0, P1, P2, P3);         \
-    accum_pair_mufu(lo2(R), ya, Q0, Q1, Q2, Q3);         \
-    accum_pair_mufu(hi2(R), yb, Q0, Q1, Q2, Q3);
-#define PC_ADJ2_ADV                                      \
-    xa = fadd2(xa, mD0);                                 \
-    xb = fadd2(xb, mD0);                                 \
-    ya = fadd2(ya, mD1);                                 \
-    yb = fadd2(yb, mD1);
-    int n = (je1 - j + LSTRIDE - 1) / LSTRIDE;
-    for (; n >= ADJ_CHUNK; n -= ADJ_CHUNK, j += ADJ_CHUNK * LSTRIDE) {
-        float4 rr[ADJ_CHUNK];
-#pragma unroll
-        for (int u = 0; u < ADJ_CHUNK; ++u) rr[u] = load_quad<ALIGNED>(row, j + u * LSTRIDE, T);
-#pragma unroll
-        for (int u = 0; u < ADJ_CHUNK; ++u) {
-            PC_ADJ2_STEP(rr[u])
-            PC_ADJ2_ADV
-        }
-    }
-    if (n > 0) {
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 q0 = load_quad<ALIGNED>(row, j, T);
-        const float4 q1 = n > 1 ? load_quad<ALIGNED>(row, j + LSTRIDE, T) : z;
-        const float4 q2 = n > 2 ? load_quad<ALIGNED>(row, j + 2 * LSTRIDE, T) : z;
-        PC_ADJ2_STEP(q0)
-        if (n > 1) {
-            PC_ADJ2_ADV
-            PC_ADJ2_STEP(q1)
-        }
-        if (n > 2) {
-            PC_ADJ2_ADV
-            PC_ADJ2_STEP(q2)
-        }
-    }
-#undef PC_ADJ2_STEP
-#undef PC_ADJ2_ADV
-}
-
-// fold one pair's moments into the ball's five accumulators
-__device__ __forceinline__ void adj_fold(float2 A0, float2 A1, float2 A2, float2 A3, float4 r0,
-                                         float4 r1, float4 r2, float& g0, float& g1, float& g2,
-                                         float& g3, float& g4) {
-    const float a1 = A1.x + A1.y, a3 = A3.x + A3.y;
-    const float aq = fmaf(A2.x + A2.y, -kKappa, A0.x + A0.y);
-    const float accR = fmaf(r1.y, a1, r1.z * aq);
-    g0 = fmaf(r1.x, a3, g0);
-    g1 = fmaf(r0.w, a1, g1);
-    g2 = fmaf(accR, r1.w, g2);
-    g3 = fmaf(accR, r2.x, g3);
-    g4 = fmaf(accR, r2.y, g4);
-}
-
-#ifndef PC_ADJ2_MINB
-#define PC_ADJ2_MINB 0
-#endif
-#if PC_ADJ2_MINB > 0
-#define PC_ADJ2_LB __launch_bounds__(ADJ_WARPS * 32, PC_ADJ2_MINB)
-#else
-#define PC_ADJ2_LB __launch_bounds__(ADJ_WARPS * 32)
-#endif
-template <bool ALIGNED, bool SPLIT>
-__global__ void PC_ADJ2_LB k_adjoint2(AdjArgs a) {
-    __shared__ __align__(16) float4 recs[ADJ_WARPS][2][32][3];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b0 = ((int64_t)blockIdx.x * ADJ_WARPS + warp) * 2;
-    const int f = SPLIT ? (int)(blockIdx.y >> 1) : (int)blockIdx.y;
-    const int m_lo = SPLIT ? (int)(blockIdx.y & 1) * a.msplit : 0;
-    const int m_hi = SPLIT ? ((blockIdx.y & 1) ? a.M : min(a.M, a.msplit)) : a.M;
-    const bool live0 = b0 < a.B, live1 = b0 + 1 < a.B;
-    const int T = a.ac.T;
-    // per-ball constants (a dead ball reads the last live one and is masked)
-    float vsb[2], Db[2], kab[2], pvb[2], inv_sb[2], sb_[2];
-    double mxb[2], myb[2], mzb[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int64_t b = min(b0 + u, a.B - 1);
-        const size_t q = (size_t)f * a.B + b;
-        mxb[u] = a.mu[3 * q + 0];
-        myb[u] = a.mu[3 * q + 1];
-        mzb[u] = a.mu[3 * q + 2];
-        const float av = a.a0[q];
-        pvb[u] = a.p0[q];
-        sb_[u] = scale_of(av);
-        vsb[u] = a.ac.vdt * sb_[u];
-        inv_sb[u] = 1.f / sb_[u];
-        kab[u] = pvb[u] / (av * av * av) * inv_sb[u] * inv_sb[u] * inv_sb[u];
-        Db[u] = (float)LSTRIDE * vsb[u];
-    }
-    const bool fast = !a.ac.exact;
-    float g[2][5];
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int c = 0; c < 5; ++c) g[u][c] = 0.f;
-    const int grp = lane / LG, sub = lane % LG;
-
-    const float* rblk = a.resid + ((size_t)f * a.M + m_lo) * T;
-    for (int mb = m_lo; mb < m_hi; mb += 32, rblk += (size_t)32 * T) {
-        const int m = mb + lane;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const bool live = u ? live1 : live0;
-            int win = -1, wh = 0, jr = 0;
-            float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
-            float ux = 0.f, uy = 0.f, uz = 0.f;
-            if (live && m < m_hi) {
-                const double dx = mxb[u] - a.pos[3 * m + 0];
-                const double dy = myb[u] - a.pos[3 * m + 1];
-                const double dz = mzb[u] - a.pos[3 * m + 2];
-                const float av = a.a0[(size_t)f * a.B + b0 + u];
-                PairSetup q;
-                pair_setup(dx, dy, dz, av, sb_[u], a.ac, 0, T, q);
-                if (q.R < kCoincidenceEps) {
-                    atomicMin(a.coinc, ((a.fo + f) * a.B + b0 + u) * a.mt + a.so + m);
-                } else if (q.jh > q.jl) {
-                    win = q.jl | (q.near ? 1 << 30 : 0);
-                    wh = q.jh;
-                    jr = q.jr;
-                    X = q.X;
-                    Y = q.Y;
-                    const double ir = 1.0 / q.R;
-                    const float inv2R = (float)(0.5 * ir);
-                    kp = inv2R * inv_sb[u];
-                    ka = kab[u] * inv2R;
-                    kR2 = pvb[u] * inv2R;
-                    kR1 = -kR2 * (float)ir * inv_sb[u];
-                    ux = (float)(dx * ir);
-                    uy = (float)(dy * ir);
-                    uz = (float)(dz * ir);
-                }
-            }
-            recs[warp][u][lane][0] = make_float4(__int_as_float(win), __int_as_float(jr), X, kp);
-            recs[warp][u][lane][1] = make_float4(ka, kR1, kR2, ux);
-            recs[warp][u][lane][2] = make_float4(uy, uz, Y, __int_as_float(wh));
-        }
-        __syncwarp();
-        const int npair = min(32, m_hi - mb);
-        for (int pb = 0; pb < npair; pb += NGRP) {
-            const int pi = pb + grp;
-            if (pi >= npair) continue;
-            const float* row = rblk + (size_t)pi * T;
-            const float4 p0r = recs[warp][0][pi][0], q0r = recs[warp][1][pi][0];
-            const int w0 = __float_as_int(p0r.x), w1 = __float_as_int(q0r.x);
-            const int h0 = __float_as_int(recs[warp][0][pi][2].w);
-            const int h1 = __float_as_int(recs[warp][1][pi][2].w);
-            bool two = fast && w0 >= 0 && w1 >= 0 && !((w0 | w1) & (1 << 30));
-            int jl = 0, jh = 0;
-            if (two) {
-                jl = min(w0, w1);
-                jh = max(h0, h1);
-                two = 2 * (jh - jl) <= (h0 - w0) + (h1 - w1) + PC_ADJ2_SLACK;
-            }
-            float2 P0 = splat2(0.f), P1 = P0, P2 = P0, P3 = P0;
-            float2 Q0 = P0, Q1 = P0, Q2 = P0, Q3 = P0;
-            if (two) {
-                adj_sweep_two<ALIGNED>(row, T, sub, jl, jh, __float_as_int(p0r.y), p0r.z, vsb[0],
-                                       __float_as_int(q0r.y), q0r.z, vsb[1], P0, P1, P2, P3, Q0,
-                                       Q1, Q2, Q3);
-            } else {
-                if (w0 >= 0)
-                    adj_sweep_one<ALIGNED>(row, T, sub, p0r, h0, fast, vsb[0], Db[0],
-                                           recs[warp][0][pi][2].z, P0, P1, P2, P3);
-                if (w1 >= 0)
-                    adj_sweep_one<ALIGNED>(row, T, sub, q0r, h1, fast, vsb[1], Db[1],
-                                           recs[warp][1][pi][2].z, Q0, Q1, Q2, Q3);
-            }
-            if (w0 >= 0)
-                adj_fold(P0, P1, P2, P3, p0r, recs[warp][0][pi][1], recs[warp][0][pi][2],
-                         g[0][0], g[0][1], g[0][2], g[0][3], g[0][4]);
-            if (w1 >= 0)
-                adj_fold(Q0, Q1, Q2, Q3, q0r, recs[warp][1][pi][1], recs[warp][1][pi][2],
-                         g[1][0], g[1][1], g[1][2], g[1][3], g[1][4]);
-        }
-        __syncwarp();
-        __syncthreads();   // the CTA's balls read the same sensor rows together
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        if (!(u ? live1 : live0)) continue;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) g[u][c] = warp_sum(g[u][c]);
-        if (lane == 0) {
-            float* out = a.G + 5 * ((size_t)f * a.B + b0 + u);
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                if (SPLIT)
-                    atomicAdd(out + c, g[u][c]);
-                else
-                    out[c] = g[u][c];
-            }
-        }
-    }
-}
-
 #if PC_ADJ_TMA
 // ---------------------------------------------------------------- adjoint,
 // TMA-staged residual windows (PC_ADJ_TMA)
@@ -2054,17 +1737,6 @@ static int adj_split() {
     return v;
 }
 
-// Two balls per warp (k_adjoint2) when PC_ADJ2=1 (environment or build
-// macro); the one-ball k_adjoint is the default (measured faster).
-static bool adj2() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("PC_ADJ2");
-        v = e ? atoi(e) != 0 : PC_ADJ2;
-    }
-    return v != 0;
-}
-
 extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, const float* p0_t,
                                        int64_t n_balls, int32_t n_frames,
                                        const pc_array_t* array, const float* residual, float* G,
@@ -2112,8 +1784,6 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
 #endif
     // few waves of 8-CTA SMs: split each ball's sensors over two CTAs (G
     // zeroed, two partial sums added)
-    const int bpc = adj2() ? 2 * ADJ_WARPS : ADJ_WARPS;   // balls per CTA
-    grid.x = (unsigned)((n_balls + bpc - 1) / bpc);
     const int64_t ctas = (int64_t)grid.x * n_frames;
     const bool split = adj_split() > 0 && a.M >= 64 && ctas < (int64_t)adj_split() * 8 * num_sms();
     a.msplit = ((a.M / 2 + 31) / 32) * 32;
@@ -2122,21 +1792,10 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
         if (cudaMemsetAsync(G, 0, (size_t)n_balls * n_frames * 5 * sizeof(float), st) != cudaSuccess)
             return PC_ERR_CUDA;
         dim3 g2(grid.x, 2 * n_frames);
-        if (adj2()) {
-            if (aligned)
-                k_adjoint2<true, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
-            else
-                k_adjoint2<false, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
-        } else if (aligned) {
-            k_adjoint<true, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
-        } else {
-            k_adjoint<false, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
-        }
-    } else if (adj2()) {
         if (aligned)
-            k_adjoint2<true, false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+            k_adjoint<true, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
         else
-            k_adjoint2<false, false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
+            k_adjoint<false, true><<<g2, ADJ_WARPS * 32, 0, st>>>(a);
     } else if (aligned) {
         k_adjoint<true, false><<<grid, ADJ_WARPS * 32, 0, st>>>(a);
     } else {
