@@ -39,19 +39,30 @@ def frame_shard(selected, rank: int, world: int) -> np.ndarray:
 
 def allreduce_iteration(grads, loss, coincident, group=None) -> None:
     """The iteration's exchange: SUM of the flat gradient buffer and of the
-    loss, MIN of the coincidence flag (pair index, INT64_MAX = none).
-    In place; works for NCCL (device tensors) and gloo (CPU tensors).
+    loss, MIN of the coincidence word (INT64_MAX = none).  In place; works
+    for NCCL (device tensors) and gloo (CPU tensors).
 
-    Three small collectives per iteration, none of which the host waits on:
-    the f32 gradients (SUM), the f64 loss (SUM) and the int64 coincidence
-    pair index (MIN).  The host reads the results once, with the rest of the
-    iteration's status after the guarded update, so the exchange adds no
-    host synchronisation of its own."""
+    Two collectives per iteration, none of which the host waits on: the f32
+    gradients (all-reduce SUM) and a 16-byte status record per rank
+    (all-gather of [loss bits, coincidence word] as int64), reduced on every
+    rank in rank order -- the loss SUM and the coincidence MIN are identical
+    on all ranks.  The host reads the results once, with the rest of the
+    iteration's status after the guarded update."""
+    import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return
-    if dist.get_world_size(group) == 1:
+    world = dist.get_world_size(group)
+    if world == 1:
         return
     dist.all_reduce(grads, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(coincident, op=dist.ReduceOp.MIN, group=group)
+    status = torch.stack([loss.reshape(1).view(torch.int64)[0],
+                          coincident.reshape(1)[0]])
+    gathered = torch.empty((world, 2), dtype=torch.int64, device=status.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, status, group=group)
+    else:
+        dist.all_gather(list(gathered.unbind(0)), status, group=group)
+    loss.copy_(gathered[:, 0].contiguous().view(torch.float64).sum()
+               .reshape(loss.shape))
+    coincident.copy_(gathered[:, 1].min().reshape(coincident.shape))
