@@ -163,11 +163,16 @@ class IterationEngine:
         self.layout = ParamLayout(B, N, self.basis, per_channel)
         self.B, self.N = B, N
         f64 = dict(dtype=torch.float64, device=self.device)
-        self.P = torch.empty(self.layout.total, **f64)
-        self.Mo = torch.zeros(self.layout.total, **f64)
-        self.Vo = torch.zeros(self.layout.total, **f64)
-        self.Gf = torch.zeros(self.layout.total, dtype=torch.float32,
-                              device=self.device)
+        # capacity-backed ball-count buffers (config-5 growth: densify
+        # re-views them instead of re-allocating; _ball_hint = growth cap)
+        self._caps = {}
+        self._ball_hint = 0
+        self._pp = 0          # which half of the ping-pong parameter storage
+        per_ball = self.layout.total // max(B, 1)
+        self.P = self._cap_view("P0", per_ball, B, torch.float64)
+        self.Mo = self._cap_view("M0", per_ball, B, torch.float64).zero_()
+        self.Vo = self._cap_view("V0", per_ball, B, torch.float64).zero_()
+        self.Gf = self._cap_view("Gf", per_ball, B, torch.float32).zero_()
         self.params = self.layout.views(self.P)
         self.grads = self.layout.views(self.Gf)
         # internal ball order (identity or Morton); outputs are un-permuted
@@ -240,6 +245,21 @@ class IterationEngine:
         self._graph = None
 
     # ------------------------------------------------------------ buffers
+    def _cap_view(self, name: str, per_ball: int, B: int, dtype):
+        """The first per_ball*B elements of a buffer sized for the ball
+        capacity (max(B, growth cap)); re-allocated only when B outgrows
+        it (by 25 %)."""
+        n = int(per_ball) * int(B)
+        t = self._caps.get(name)
+        if t is None or t.dtype != dtype or t.numel() < n:
+            cap = max(int(B), int(self._ball_hint), 1)
+            if t is not None and t.numel() < n:
+                cap = max(cap, int(B + B // 4))
+            self._caps[name] = None
+            t = torch.empty(int(per_ball) * cap, dtype=dtype, device=self.device)
+            self._caps[name] = t
+        return t[:n]
+
     def _ensure_buffers(self, F: int):
         if (self._bufs_F == F and self.mu_t is not None
                 and self.mu_t.shape[1] == self.B):
@@ -253,11 +273,14 @@ class IterationEngine:
             self.loss_f = torch.zeros(F, dtype=torch.float64, device=dev)
             self.obs_stage = None
             self.loss_part = torch.empty(F * M, dtype=torch.float64, device=dev)
-        self.mu_t = torch.empty((F, B, 3), dtype=torch.float64, device=dev)
-        self.a0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
-        self.p0_t = torch.empty((F, B), dtype=torch.float32, device=dev)
-        self.H = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
-        self.G = torch.empty((F, B, 5), dtype=torch.float32, device=dev)
+        if self._bufs_F != F:
+            for k in ("mu_t", "a0_t", "p0_t", "H", "G"):
+                self._caps.pop(k, None)
+        self.mu_t = self._cap_view("mu_t", 3 * F, B, torch.float64).view(F, B, 3)
+        self.a0_t = self._cap_view("a0_t", F, B, torch.float32).view(F, B)
+        self.p0_t = self._cap_view("p0_t", F, B, torch.float32).view(F, B)
+        self.H = self._cap_view("H", 5 * F, B, torch.float32).view(F, B, 5)
+        self.G = self._cap_view("G", 5 * F, B, torch.float32).view(F, B, 5)
         ws = self.darr.workspace_bytes(max(B, 1), F)
         if self.ws is None or self.ws.numel() < ws:
             # 25 % headroom: a growing cloud (densify) re-allocates the
@@ -756,10 +779,14 @@ class IterationEngine:
         index = index[:B2]
         per_channel = self.basis == "gauss" and self.params["theta"].dim() == 3
         layout = ParamLayout(B2, self.N, self.basis, per_channel)
-        f64 = dict(dtype=torch.float64, device=dev)
-        P2 = torch.empty(layout.total, **f64)
-        M2 = torch.empty(layout.total, **f64)
-        V2 = torch.empty(layout.total, **f64)
+        if max_balls is not None:
+            self._ball_hint = max(self._ball_hint, int(max_balls))
+        # the other half of the ping-pong parameter / moment storage
+        per_ball = layout.total // max(B2, 1)
+        side = 1 - self._pp
+        P2 = self._cap_view(f"P{side}", per_ball, B2, torch.float64)
+        M2 = self._cap_view(f"M{side}", per_ball, B2, torch.float64)
+        V2 = self._cap_view(f"V{side}", per_ball, B2, torch.float64)
         for old, new in zip(self.layout.segments, layout.segments):
             row = (old.size // B) * 8
             for src, dst in ((self.P, P2), (self.Mo, M2), (self.Vo, V2)):
@@ -786,7 +813,9 @@ class IterationEngine:
         # swap in the new cloud (internal order becomes the caller's order)
         self.layout, self.B = layout, B2
         self.P, self.Mo, self.Vo = P2, M2, V2
-        self.Gf = torch.zeros(layout.total, dtype=torch.float32, device=dev)
+        self._pp = side
+        self.Gf = self._cap_view("Gf", per_ball, B2, torch.float32)
+        self.Gf.zero_()
         self.params = layout.views(self.P)
         self.grads = layout.views(self.Gf)
         p = self.params
