@@ -129,7 +129,8 @@ struct FrSmem {
     static constexpr size_t recB = recA + (size_t)FR_CHUNK * 16;         // u32 [C]: jl | jh << 16
     static constexpr size_t recY = recB + (size_t)FR_CHUNK * 4;          // f32 [C]: near-field Y
     static constexpr size_t gspan = recY + (size_t)FR_CHUNK * 4;         // u32 [C/32]
-    static constexpr size_t queue = gspan + (size_t)FR_GROUPS * 4;       // u16 [W][QLEN]
+    static constexpr size_t gfull = gspan + (size_t)FR_GROUPS * 4;       // u32 [C/32]: runs every member meets
+    static constexpr size_t queue = gfull + (size_t)FR_GROUPS * 4;       // u16 [W][QLEN]
     static constexpr size_t xbuf = queue + (size_t)FR_WARPS * FR_QLEN * 2;   // f32 [W][32][XPAD]
     static constexpr size_t ctl = xbuf + (size_t)FR_WARPS * 32 * FR_XPAD * 4; // int [8]
     static constexpr size_t trace = ctl + 64;                            // f32 [Tpad]
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
     unsigned* recB = reinterpret_cast<unsigned*>(sm + FrSmem::recB);
     float* recY = reinterpret_cast<float*>(sm + FrSmem::recY);
     unsigned* gspan = reinterpret_cast<unsigned*>(sm + FrSmem::gspan);
+    unsigned* gfull = reinterpret_cast<unsigned*>(sm + FrSmem::gfull);
     unsigned short* queue = reinterpret_cast<unsigned short*>(sm + FrSmem::queue);
     float* xbuf = reinterpret_cast<float*>(sm + FrSmem::xbuf);
     int* ctl = reinterpret_cast<int*>(sm + FrSmem::ctl);
@@ -457,9 +459,13 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             const int jl = wb & 0xffff, jh = wb >> 16;
             const int q0 = __reduce_min_sync(0xffffffffu, jh > jl ? jl / FR_RUN : 0x7fff);
             const int q1 = __reduce_max_sync(0xffffffffu, jh > jl ? (jh - 1) / FR_RUN : -1);
+            // runs that every member's window meets (all 32 live): [max q0, min q1]
+            const int f0 = __reduce_max_sync(0xffffffffu, jh > jl ? jl / FR_RUN : 0x7fff);
+            const int f1 = __reduce_min_sync(0xffffffffu, jh > jl ? (jh - 1) / FR_RUN : -1);
             const int g = i >> 5;
             if (lane == 0) {
                 gspan[g] = q1 >= q0 ? ((unsigned)q0 | ((unsigned)q1 << 16)) : 0x0000ffffu;
+                gfull[g] = f1 >= f0 ? ((unsigned)f0 | ((unsigned)f1 << 16)) : 0x0000ffffu;
                 if (q1 >= q0) {
                     atomicMin(cc + 1, q0);
                     atomicMax(cc + 2, q1);
@@ -539,6 +545,32 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                 const unsigned sp = gspan[gb + lane];
                 const bool gh = (int)(sp & 0xffff) <= q && q <= (int)(sp >> 16);
                 unsigned gm = __ballot_sync(0xffffffffu, gh);
+#if PC_FR_DIRECT
+                {
+                    // groups every member of which meets the run: swept
+                    // directly without testing the members' windows
+                    const unsigned fu = gfull[gb + lane];
+                    const unsigned fm = __ballot_sync(
+                        0xffffffffu, (int)(fu & 0xffff) <= q && q <= (int)(fu >> 16));
+                    gm &= ~fm;
+                    unsigned fl = fm;
+                    while (fl) {
+                        const int g = gb + __ffs(fl) - 1;
+                        fl &= fl - 1;
+                        const int i = g * 32 + lane;
+                        const float4 r = recA[i];
+                        const int w = __float_as_int(r.w);
+                        if (!(w & (1 << 30))) {
+                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                        } else {
+                            const unsigned wq = recB[i];
+                            fr_slow(acc, j0, r.x, recY[i], r.z, r.y, w & 0xffff, wq & 0xffff,
+                                    wq >> 16, w < 0);
+                        }
+                        nd = 1;
+                    }
+                }
+#endif
                 while (gm) {
                     const int g = gb + __ffs(gm) - 1;
                     gm &= gm - 1;
