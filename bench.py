@@ -269,7 +269,8 @@ def run_reference(args, rank, world):
     prob = synth.make_problem(args.config, seed=args.seed, basis=args.basis,
                               n_basis=args.n_basis)
     threads = os.cpu_count() or 1
-    n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
+    # ~1.3 s of 16-thread work per step at config 3 (13 steps: ~17 s)
+    n_s = args.cpu_sensors or {3: 32, 4: 8, 5: 32}.get(args.config, 128)
     samp = CpuSample(prob, n_s, threads)
     for _ in range(max(1, args.warmup)):
         samp.time_once()
@@ -529,7 +530,8 @@ def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        n_s = args.cpu_sensors or (16 if args.config >= 3 else 32)
+        # ~5 s of 16-thread work per pass at config 3 (3 passes: ~15 s)
+        n_s = args.cpu_sensors or {3: 128, 4: 32, 5: 128}.get(args.config, 512)
         samp = CpuSample(prob, n_s, threads,
                          full_support=full_support_initial(prob, dev))
         samp.time_once()

@@ -164,6 +164,13 @@ int pc_deform_backward(const pc_cloud_t *cloud, const double *t_frames_dev,
 int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array_t *array,
                     int32_t *plan);
 
+/* Which forward kernel pc_forward_traces runs for this array: 0 = register-run
+ * forward (default), 1 = shared-memory-trace forward (PC_FWD_LEGACY=1 or a
+ * trace too long for the run kernel), 2 = register-run forward with the ball
+ * tiles staged by cp.async.bulk (TMA) behind an mbarrier (PC_FWD_TMA=1).  All
+ * three replace radiator.py:86-118.  -1 for a NULL array. */
+int pc_forward_variant(const pc_array_t *array);
+
 /* Scratch bytes pc_forward_traces needs for this problem (0 = none). */
 size_t pc_forward_workspace_bytes(int64_t n_balls, int32_t n_frames,
                                   const pc_array_t *array);

@@ -67,6 +67,7 @@ SIGNATURES = {
                                      _P]),
     "pc_forward_plan": (c_int32, [c_int64, c_int32, POINTER(PcArray),
                                   POINTER(c_int32)]),
+    "pc_forward_variant": (c_int32, [POINTER(PcArray)]),
     "pc_forward_workspace_bytes": (c_size_t, [c_int64, c_int32,
                                               POINTER(PcArray)]),
     "pc_forward_traces": (c_int32, [_P, _P, _P, c_int64, c_int32,

@@ -158,5 +158,15 @@ int fwd_run_launch(const double* mu_t, const float* a0_t, const float* p0_t, int
                    int32_t F, const pc_array_t* array, const ArrayConsts& ac,
                    const float* observed, float* out, double* loss_partial,
                    int64_t* coincident, cudaStream_t st);
+// the same file compiled with TMA-staged ball tiles (PC_FWD_TMA=1 at run time)
+namespace tma {
+int fwd_run_supported(const pc_array_t* array);
+int fwd_run_samples_per_run();
+size_t fwd_run_workspace_bytes(int32_t n_frames, const pc_array_t* array);
+int fwd_run_launch(const double* mu_t, const float* a0_t, const float* p0_t, int64_t n_balls,
+                   int32_t F, const pc_array_t* array, const ArrayConsts& ac,
+                   const float* observed, float* out, double* loss_partial,
+                   int64_t* coincident, cudaStream_t st);
+}  // namespace tma
 
 }  // namespace pc

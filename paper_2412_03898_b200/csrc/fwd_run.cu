@@ -47,7 +47,13 @@
 
 #include "common.cuh"
 
+// The file is compiled twice into the library: as is (the default forward)
+// and with -DPC_FR_NS=tma -DPC_FR_TMA=1 -DPC_FR_CHUNK=512 (the TMA-staged
+// variant, selected at run time with PC_FWD_TMA=1), each in its own namespace.
 namespace pc {
+#ifdef PC_FR_NS
+namespace PC_FR_NS {
+#endif
 
 #ifndef PC_FR_RUN
 #define PC_FR_RUN 32
@@ -84,6 +90,28 @@ namespace pc {
 #ifndef PC_FR_MINB
 #define PC_FR_MINB 4
 #endif
+// PC_FR_SEEDS 1: the fast path takes the per-ball constant u = 2^(-D^2)
+// (D = 2 s v dt) from the setup pass (kept in the record's Y word, which only
+// near-field pairs use): h = u^2 and g(x - s v dt) = g(x) u, so a ball-run
+// seeds 10 MUFU instead of 13.
+#ifndef PC_FR_SEEDS
+#define PC_FR_SEEDS 0
+#endif
+// PC_FR_TMA 1: the chunk's raw ball tile (mu, a0, p0 of FR_CHUNK balls) is
+// staged in shared memory by three cp.async.bulk (TMA) copies completing on
+// an mbarrier; the copy of chunk c+1 is issued right after chunk c's setup
+// pass has consumed the stage, so it lands while the runs of chunk c are
+// swept (the stage and the record buffers are the two halves of the
+// pipeline).  Chunks whose global addresses or byte counts are not 16-byte
+// multiples fall back to plain loads.
+#ifndef PC_FR_TMA
+#define PC_FR_TMA 0
+#endif
+// PC_FR_PF 1: L1 prefetch of the next chunk's raw balls at the start of the
+// chunk's runs (the no-shared-memory counterpart of PC_FR_TMA).
+#ifndef PC_FR_PF
+#define PC_FR_PF 0
+#endif
 constexpr int FR_RUN = PC_FR_RUN;          // samples per run (register accumulators)
 constexpr int FR_CHUNK = PC_FR_CHUNK;      // balls per setup chunk
 #ifndef PC_FR_WARPS
@@ -102,6 +130,7 @@ constexpr int FR_QLEN = 64;                // per-warp ball queue (circular)
 #endif
 constexpr int FR_XPAD = PC_FR_XQ ? 9 : 20;  // transpose row stride (floats)
 constexpr float FR_SCALE_EXP = 80.f;       // chains carry c 2^(80 - x^2)
+#define FR_U(idx) (PC_FR_SEEDS ? recY[idx] : 0.f)
 
 struct FwdRunArgs {
     const double* mu;      // (F,B,3)
@@ -133,7 +162,11 @@ struct FrSmem {
     static constexpr size_t queue = gfull + (size_t)FR_GROUPS * 4;       // u16 [W][QLEN]
     static constexpr size_t xbuf = queue + (size_t)FR_WARPS * FR_QLEN * 2;   // f32 [W][32][XPAD]
     static constexpr size_t ctl = xbuf + (size_t)FR_WARPS * 32 * FR_XPAD * 4; // int [8]
-    static constexpr size_t trace = ctl + 64;                            // f32 [Tpad]
+    // TMA stage of the next chunk's raw balls: mu f64 [C][3] | a0 f32 [C] | p0 f32 [C]
+    static constexpr size_t rawmu = ctl + 64;
+    static constexpr size_t rawa = rawmu + (PC_FR_TMA ? (size_t)FR_CHUNK * 24 : 0);
+    static constexpr size_t rawp = rawa + (PC_FR_TMA ? (size_t)FR_CHUNK * 4 : 0);
+    static constexpr size_t trace = rawp + (PC_FR_TMA ? (size_t)FR_CHUNK * 4 : 0);   // f32 [Tpad]
 };
 
 // after the trace: run weights (int [Tp/RUN]), run order (u16 [Tp/RUN]),
@@ -150,7 +183,8 @@ static size_t fr_smem_bytes(int T) {
 // the other factor carries it (xc = c x, stepped by -c D), so doubling p0
 // doubles every product exactly (radiator tests: p0 scaling / two identical
 // balls are bit-exact).
-__device__ __forceinline__ void fr_fast(float2 (&acc)[FR_RUN / 2], float x0, float vs, float cs) {
+__device__ __forceinline__ void fr_fast(float2 (&acc)[FR_RUN / 2], float x0, float vs, float cs,
+                                        float u) {
     static_assert(FR_RUN == 32, "two interleaved 16-sample halves");
 #if PC_FR_CHAIN1
     // one packed chain over the whole run: 4 MUFU seeds instead of 8 (the
@@ -178,8 +212,12 @@ __device__ __forceinline__ void fr_fast(float2 (&acc)[FR_RUN / 2], float x0, flo
 #endif
     const float D = 2.f * vs;
     const float2 mcD = splat2(-cs * D);
+#if PC_FR_SEEDS
+    const float2 h2 = splat2(u * u);
+#else
     const float2 h2 = splat2(ex2(-2.f * D * D));
     const float2 tD = splat2(2.f * D), mDD = splat2(-D * D);
+#endif
     const float2 csc = splat2(cs);
     // the two halves' chains run interleaved (independent: ILP for the
     // 4-cycle FMA-pipe latency of each chain)
@@ -188,8 +226,13 @@ __device__ __forceinline__ void fr_fast(float2 (&acc)[FR_RUN / 2], float x0, flo
     const float2 xxa = fmul2(xa, xa), xxb = fmul2(xb, xb);
     float2 ea = make_float2(ex2(FR_SCALE_EXP - xxa.x), ex2(FR_SCALE_EXP - xxa.y));
     float2 eb = make_float2(ex2(FR_SCALE_EXP - xxb.x), ex2(FR_SCALE_EXP - xxb.y));
+#if PC_FR_SEEDS
+    const float gax = ex2(fmaf(xa.x, 2.f * D, -D * D)), gbx = ex2(fmaf(xb.x, 2.f * D, -D * D));
+    float2 ga = make_float2(gax, gax * u), gb = make_float2(gbx, gbx * u);
+#else
     float2 ga = ex2_2(ffma2(xa, tD, mDD));
     float2 gb = ex2_2(ffma2(xb, tD, mDD));
+#endif
     float2 ca = fmul2(csc, xa), cb = fmul2(csc, xb);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -363,6 +406,36 @@ __device__ __forceinline__ void fr_epilogue(const FwdRunArgs& a, const float* tr
     }
 }
 
+#if PC_FR_TMA
+__device__ __forceinline__ unsigned fr_smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void fr_mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(fr_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fr_mbar_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fr_smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void fr_mbar_wait(unsigned long long* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(fr_smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fr_bulk(void* dst, const void* src, unsigned bytes,
+                                        unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(fr_smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(fr_smem_u32(bar))
+        : "memory");
+}
+#endif
+
 template <bool EXACT>
 __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -396,6 +469,34 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
     __syncthreads();
 
     const size_t fb = (size_t)f * a.B;
+#if PC_FR_TMA
+    const double* rawmu = reinterpret_cast<const double*>(sm + FrSmem::rawmu);
+    const float* rawa = reinterpret_cast<const float*>(sm + FrSmem::rawa);
+    const float* rawp = reinterpret_cast<const float*>(sm + FrSmem::rawp);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(ctl + 8);
+    // a chunk is staged when its three sources are 16-byte aligned whole
+    // multiples of 16 bytes (always, for full chunks of aligned frames)
+    auto stageable = [&](int64_t c) -> bool {
+        const int64_t n = min((int64_t)FR_CHUNK, a.B - c);
+        return ((reinterpret_cast<uintptr_t>(a.mu + 3 * (fb + c)) |
+                 reinterpret_cast<uintptr_t>(a.a0 + fb + c) |
+                 reinterpret_cast<uintptr_t>(a.p0 + fb + c)) & 15) == 0 && (n & 3) == 0;
+    };
+    auto stage = [&](int64_t c) {
+        const unsigned n = (unsigned)min((int64_t)FR_CHUNK, a.B - c);
+        fr_mbar_expect(bar, n * 32u);
+        fr_bulk(sm + FrSmem::rawmu, a.mu + 3 * (fb + c), n * 24u, bar);
+        fr_bulk(sm + FrSmem::rawa, a.a0 + fb + c, n * 4u, bar);
+        fr_bulk(sm + FrSmem::rawp, a.p0 + fb + c, n * 4u, bar);
+    };
+    unsigned phase = 0;
+    if (tid == 0) {
+        fr_mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (a.B > 0 && stageable(0)) stage(0);
+    }
+    __syncthreads();
+#endif
     const unsigned lt = (1u << lane) - 1u;
     unsigned short* Q = queue + warp * FR_QLEN;
     float* xb = xbuf + warp * 32 * FR_XPAD;
@@ -403,6 +504,13 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
     for (int64_t c0 = 0; c0 < a.B; c0 += FR_CHUNK, par ^= 1) {
         int* cc = ctl + 4 * par;
         // ---------------------------------------------------------- setup
+#if PC_FR_TMA
+        const bool staged = stageable(c0);
+        if (staged) {
+            fr_mbar_wait(bar, phase);
+            phase ^= 1u;
+        }
+#endif
         for (int i = tid; i < FR_CHUNK; i += FR_THREADS) {
             const int64_t b = c0 + i;
             unsigned wb = 0x0000ffffu;           // empty window (jl = 0xffff, jh = 0)
@@ -410,8 +518,16 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             float ry = 0.f;
             if (b < a.B) {
                 const size_t s3 = 3 * (fb + b);
+#if PC_FR_TMA
+                const double dx = (staged ? rawmu[3 * i] : a.mu[s3]) - px;
+                const double dy = (staged ? rawmu[3 * i + 1] : a.mu[s3 + 1]) - py;
+                const double dz = (staged ? rawmu[3 * i + 2] : a.mu[s3 + 2]) - pz;
+                const float av = staged ? rawa[i] : a.a0[fb + b];
+                const float pv = staged ? rawp[i] : a.p0[fb + b];
+#else
                 const double dx = a.mu[s3] - px, dy = a.mu[s3 + 1] - py, dz = a.mu[s3 + 2] - pz;
                 const float av = a.a0[fb + b];
+#endif
                 const float s = __fdividef(sqrtf(kHalfLog2e), av);
                 const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
                 const float r2f = (float)R2;
@@ -444,7 +560,14 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                         const bool near = (float)R + a.vt0_f + a.vdt_f * (float)lo < 10.f * av;
                         const float vs = a.vdt_f * s;
                         const bool fast = !EXACT && !near && vs <= a.vs_max;
+#if PC_FR_TMA
+                        const float cs = __fdividef(0.5f * pv, (float)R * s);
+#else
                         const float cs = __fdividef(0.5f * a.p0[fb + b], (float)R * s);
+#endif
+#if PC_FR_SEEDS
+                        if (fast) ry = ex2(-4.f * vs * vs);   // u = 2^(-D^2), D = 2 vs
+#endif
                         ra = make_float4(X, cs, vs,
                                          __int_as_float(jr | (fast ? 0 : 1 << 30) |
                                                         (near ? (int)0x80000000u : 0)));
@@ -485,6 +608,23 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             cn[2] = -1;
         }
         __syncthreads();
+#if PC_FR_TMA
+        // the stage is consumed: start the next chunk's copy under this
+        // chunk's runs
+        if (tid == 0 && c0 + FR_CHUNK < a.B && stageable(c0 + FR_CHUNK)) stage(c0 + FR_CHUNK);
+#endif
+#if PC_FR_PF
+        for (int i = tid; i < FR_CHUNK; i += FR_THREADS) {
+            const int64_t b = c0 + FR_CHUNK + i;
+            if (b < a.B) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.mu + 3 * (fb + b)));
+                if ((i & 31) == 0) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.a0 + fb + b));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a.p0 + fb + b));
+                }
+            }
+        }
+#endif
         const int rlo = cc[1], rhi = cc[2];
         const int nrun = rhi - rlo + 1;
         // ---------------------------------------------------------- task order
@@ -542,14 +682,17 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             for (int k = 0; k < FR_RUN / 2; ++k) acc[k] = splat2(0.f);
             int qn = 0, qd = 0, nd = 0;   // nd: a full group went the direct way
             for (int gb = 0; gb < FR_GROUPS; gb += 32) {
-                const unsigned sp = gspan[gb + lane];
+                const unsigned sp = (FR_GROUPS % 32 == 0 || gb + lane < FR_GROUPS) ? gspan[gb + lane]
+                                                                                : 0x0000ffffu;
                 const bool gh = (int)(sp & 0xffff) <= q && q <= (int)(sp >> 16);
                 unsigned gm = __ballot_sync(0xffffffffu, gh);
 #if PC_FR_DIRECT
                 {
                     // groups every member of which meets the run: swept
                     // directly without testing the members' windows
-                    const unsigned fu = gfull[gb + lane];
+                    const unsigned fu = (FR_GROUPS % 32 == 0 || gb + lane < FR_GROUPS)
+                                            ? gfull[gb + lane]
+                                            : 0x0000ffffu;
                     const unsigned fm = __ballot_sync(
                         0xffffffffu, (int)(fu & 0xffff) <= q && q <= (int)(fu >> 16));
                     gm &= ~fm;
@@ -561,7 +704,8 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                         const float4 r = recA[i];
                         const int w = __float_as_int(r.w);
                         if (!(w & (1 << 30))) {
-                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y,
+                                    FR_U(i));
                         } else {
                             const unsigned wq = recB[i];
                             fr_slow(acc, j0, r.x, recY[i], r.z, r.y, w & 0xffff, wq & 0xffff,
@@ -587,7 +731,8 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                         const float4 r = recA[i];
                         const int w = __float_as_int(r.w);
                         if (!(w & (1 << 30))) {
-                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y,
+                                    FR_U(i));
                         } else {
                             fr_slow(acc, j0, r.x, recY[i], r.z, r.y, w & 0xffff, wb & 0xffff,
                                     wb >> 16, w < 0);
@@ -605,7 +750,8 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                         const float4 r = recA[e];
                         const int w = __float_as_int(r.w);
                         if (!(w & (1 << 30))) {
-                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                            fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y,
+                                    FR_U(e));
                         } else {
                             const unsigned wq = recB[e];
                             fr_slow(acc, j0, r.x, recY[e], r.z, r.y, w & 0xffff, wq & 0xffff,
@@ -621,7 +767,8 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                 const float4 r = recA[e];
                 const int w = __float_as_int(r.w);
                 if (!(w & (1 << 30))) {
-                    fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y);
+                    fr_fast(acc, fmaf(-(float)(j0 - (w & 0xffff)), r.z, r.x), r.z, r.y,
+                            FR_U(e));
                 } else {
                     const unsigned wq = recB[e];
                     fr_slow(acc, j0, r.x, recY[e], r.z, r.y, w & 0xffff, wq & 0xffff, wq >> 16,
@@ -704,4 +851,7 @@ int fwd_run_launch(const double* mu_t, const float* a0_t, const float* p0_t, int
     return last_status();
 }
 
+#ifdef PC_FR_NS
+}  // namespace PC_FR_NS
+#endif
 }  // namespace pc

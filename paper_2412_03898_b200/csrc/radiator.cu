@@ -1547,6 +1547,20 @@ static bool fwd_legacy(const pc_array_t* array) {
     return v != 0 || !fwd_run_supported(array);
 }
 
+// PC_FWD_TMA=1: the register-run forward with the chunk's raw ball tile
+// staged in shared memory by cp.async.bulk behind an mbarrier (fwd_run.cu
+// compiled with PC_FR_TMA; chunks of 512 balls so four CTAs still fit an SM).
+// Measured 7 % slower than the default on config 3:
+// kept selectable and parity-tested.
+static bool fwd_tma(const pc_array_t* array) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("PC_FWD_TMA");
+        v = e ? atoi(e) != 0 : 0;
+    }
+    return v != 0 && tma::fwd_run_supported(array);
+}
+
 extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array_t* array,
                                int32_t* plan) {
     if (!array || !plan || n_balls < 0 || n_frames < 1 || array->n_sensors < 1 ||
@@ -1566,6 +1580,11 @@ extern "C" int pc_forward_plan(int64_t n_balls, int32_t n_frames, const pc_array
     plan[2] = p.nchunk;
     plan[3] = 3 + (p.nchunk > 1 ? 1 : 0);  // prep + forward [+ combine] + loss reduce
     return PC_OK;
+}
+
+extern "C" int pc_forward_variant(const pc_array_t* array) {
+    if (!array) return -1;
+    return fwd_legacy(array) ? 1 : fwd_tma(array) ? 2 : 0;
 }
 
 extern "C" size_t pc_forward_workspace_bytes(int64_t n_balls, int32_t n_frames,
@@ -1595,8 +1614,12 @@ extern "C" int pc_forward_traces(const double* mu_t, const float* a0_t, const fl
             return PC_ERR_ARGUMENT;
         double* lpart = reinterpret_cast<double*>(workspace);
         if (n_balls > 0) {
-            const int rc = fwd_run_launch(mu_t, a0_t, p0_t, n_balls, F, array, ac, observed, out,
-                                          want_loss ? lpart : nullptr, coincident, st);
+            const int rc =
+                fwd_tma(array)
+                    ? tma::fwd_run_launch(mu_t, a0_t, p0_t, n_balls, F, array, ac, observed, out,
+                                          want_loss ? lpart : nullptr, coincident, st)
+                    : fwd_run_launch(mu_t, a0_t, p0_t, n_balls, F, array, ac, observed, out,
+                                     want_loss ? lpart : nullptr, coincident, st);
             if (rc != PC_OK) return rc;
         } else {
             if (cudaMemsetAsync(out, 0, (size_t)F * M * T * sizeof(float), st) != cudaSuccess)

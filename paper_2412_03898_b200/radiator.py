@@ -88,6 +88,12 @@ class DeviceArray:
         self.sensor_offset = int(sensor_offset)
         self.n_sensors_total = n_total
 
+    def variant(self) -> int:
+        """pc_forward_variant: 0 register-run forward, 1 legacy shared-memory
+        trace forward, 2 register-run forward with TMA-staged ball tiles."""
+        lib = _lib.load_library(require_cuda=False)
+        return int(lib.pc_forward_variant(ctypes.byref(self.struct)))
+
     def plan(self, n_balls: int, n_frames: int) -> dict:
         """pc_forward_plan: time segment, segments, ball chunks, launches."""
         lib = _lib.load_library(require_cuda=False)

@@ -12,6 +12,7 @@ FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include $DEFS"
 for f in radiator fwd_run deform optim voxel ubp; do
   nvcc $FL -c $C/$f.cu -o $OUT/$f.o &
 done
+nvcc $FL -DPC_FR_NS=tma -DPC_FR_TMA=1 -DPC_FR_CHUNK=512 -c $C/fwd_run.cu -o $OUT/fwd_run_tma.o &
 wait
 nvcc $ARCH -shared -cudart static -o $ROOT/build/variants/$NAME.so $OUT/*.o
 echo built build/variants/$NAME.so
