@@ -107,11 +107,22 @@ namespace PC_FR_NS {
 #ifndef PC_FR_TMA
 #define PC_FR_TMA 0
 #endif
+// PC_FR_DIET 1 (default): the setup pass without the libdevice range guards
+// (raw rcp / rsqrt.approx.ftz: the operands are normal floats), chunk-local
+// 32-bit indexing, and the chunk's run range reduced from the group spans
+// after the barrier instead of two shared-memory atomics per group.
+#ifndef PC_FR_DIET
+#define PC_FR_DIET 1
+#endif
+#ifndef PC_FR_SETUP_UNROLL
+#define PC_FR_SETUP_UNROLL 1
+#endif
 // PC_FR_PF 1: L1 prefetch of the next chunk's raw balls at the start of the
 // chunk's runs (the no-shared-memory counterpart of PC_FR_TMA).
 #ifndef PC_FR_PF
 #define PC_FR_PF 0
 #endif
+constexpr int FR_SETUP_UNROLL = PC_FR_SETUP_UNROLL;
 constexpr int FR_RUN = PC_FR_RUN;          // samples per run (register accumulators)
 constexpr int FR_CHUNK = PC_FR_CHUNK;      // balls per setup chunk
 #ifndef PC_FR_WARPS
@@ -131,6 +142,25 @@ constexpr int FR_QLEN = 64;                // per-warp ball queue (circular)
 constexpr int FR_XPAD = PC_FR_XQ ? 9 : 20;  // transpose row stride (floats)
 constexpr float FR_SCALE_EXP = 80.f;       // chains carry c 2^(80 - x^2)
 #define FR_U(idx) (PC_FR_SEEDS ? recY[idx] : 0.f)
+
+__device__ __forceinline__ float fr_rcp(float x) {
+#if PC_FR_DIET
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+#else
+    return __fdividef(1.f, x);
+#endif
+}
+__device__ __forceinline__ float fr_rsqrt(float x) {
+#if PC_FR_DIET
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+#else
+    return rsqrtf(x);
+#endif
+}
 
 struct FwdRunArgs {
     const double* mu;      // (F,B,3)
@@ -511,34 +541,43 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             phase ^= 1u;
         }
 #endif
+        // chunk-local views: 32-bit indices inside the chunk
+        const double* muc = a.mu + 3 * (fb + c0);
+        const float* a0c = a.a0 + fb + c0;
+        const float* p0c = a.p0 + fb + c0;
+        const int nb = (int)min((int64_t)FR_CHUNK, a.B - c0);
+#pragma unroll FR_SETUP_UNROLL
         for (int i = tid; i < FR_CHUNK; i += FR_THREADS) {
-            const int64_t b = c0 + i;
             unsigned wb = 0x0000ffffu;           // empty window (jl = 0xffff, jh = 0)
             float4 ra = make_float4(0.f, 0.f, 0.f, 0.f);
             float ry = 0.f;
-            if (b < a.B) {
-                const size_t s3 = 3 * (fb + b);
+            if (i < nb) {
 #if PC_FR_TMA
-                const double dx = (staged ? rawmu[3 * i] : a.mu[s3]) - px;
-                const double dy = (staged ? rawmu[3 * i + 1] : a.mu[s3 + 1]) - py;
-                const double dz = (staged ? rawmu[3 * i + 2] : a.mu[s3 + 2]) - pz;
-                const float av = staged ? rawa[i] : a.a0[fb + b];
-                const float pv = staged ? rawp[i] : a.p0[fb + b];
+                const double dx = (staged ? rawmu[3 * i] : muc[3 * i]) - px;
+                const double dy = (staged ? rawmu[3 * i + 1] : muc[3 * i + 1]) - py;
+                const double dz = (staged ? rawmu[3 * i + 2] : muc[3 * i + 2]) - pz;
+                const float av = staged ? rawa[i] : a0c[i];
+                const float pv = staged ? rawp[i] : p0c[i];
 #else
-                const double dx = a.mu[s3] - px, dy = a.mu[s3 + 1] - py, dz = a.mu[s3 + 2] - pz;
-                const float av = a.a0[fb + b];
+                const double dx = muc[3 * i] - px, dy = muc[3 * i + 1] - py, dz = muc[3 * i + 2] - pz;
+                const float av = a0c[i];
+                const float pv = p0c[i];
 #endif
+#if PC_FR_DIET
+                const float s = sqrtf(kHalfLog2e) * fr_rcp(av);
+#else
                 const float s = __fdividef(sqrtf(kHalfLog2e), av);
+#endif
                 const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
                 const float r2f = (float)R2;
-                const float rinv = rsqrtf(r2f);
+                const float rinv = fr_rsqrt(r2f);
                 const float rf = r2f * rinv;
                 const double R = r2f > 1e-30f
                                      ? fma(fma(-(double)rf, (double)rf, R2), 0.5 * (double)rinv,
                                            (double)rf)
                                      : sqrt(R2);
                 if (R < kCoincidenceEps) {
-                    atomicMin(a.coinc, ((a.frame_offset + f) * a.B + b) * a.n_sensors_total +
+                    atomicMin(a.coinc, ((a.frame_offset + f) * a.B + (c0 + i)) * a.n_sensors_total +
                                            a.sensor_offset + m);
                 } else {
                     const float tc = ((float)R * a.inv_v_f - a.t0_f) * a.inv_dt_f;
@@ -560,10 +599,10 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                         const bool near = (float)R + a.vt0_f + a.vdt_f * (float)lo < 10.f * av;
                         const float vs = a.vdt_f * s;
                         const bool fast = !EXACT && !near && vs <= a.vs_max;
-#if PC_FR_TMA
-                        const float cs = __fdividef(0.5f * pv, (float)R * s);
+#if PC_FR_DIET
+                        const float cs = (0.5f * pv) * fr_rcp((float)R * s);
 #else
-                        const float cs = __fdividef(0.5f * a.p0[fb + b], (float)R * s);
+                        const float cs = __fdividef(0.5f * pv, (float)R * s);
 #endif
 #if PC_FR_SEEDS
                         if (fast) ry = ex2(-4.f * vs * vs);   // u = 2^(-D^2), D = 2 vs
@@ -590,8 +629,10 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                 gspan[g] = q1 >= q0 ? ((unsigned)q0 | ((unsigned)q1 << 16)) : 0x0000ffffu;
                 gfull[g] = f1 >= f0 ? ((unsigned)f0 | ((unsigned)f1 << 16)) : 0x0000ffffu;
                 if (q1 >= q0) {
+#if !PC_FR_DIET || PC_FR_ORDER
                     atomicMin(cc + 1, q0);
                     atomicMax(cc + 2, q1);
+#endif
 #if PC_FR_ORDER
                     // run weight (groups whose span holds the run, the task
                     // order's work proxy) as a difference array
@@ -625,7 +666,26 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             }
         }
 #endif
+#if PC_FR_DIET && !PC_FR_ORDER
+        // the chunk's run range from the group spans (every warp reduces the
+        // same FR_GROUPS words: no atomics in the setup, no extra barrier)
+        int rlo, rhi;
+        {
+            int l = 0x7fff, h = -1;
+            for (int g = lane; g < FR_GROUPS; g += 32) {
+                const unsigned sp = gspan[g];
+                const int s0 = (int)(sp & 0xffff), s1 = (int)(sp >> 16);
+                if (s1 >= s0) {
+                    l = min(l, s0);
+                    h = max(h, s1);
+                }
+            }
+            rlo = __reduce_min_sync(0xffffffffu, l);
+            rhi = __reduce_max_sync(0xffffffffu, h);
+        }
+#else
         const int rlo = cc[1], rhi = cc[2];
+#endif
         const int nrun = rhi - rlo + 1;
         // ---------------------------------------------------------- task order
         // warp 0: runs by descending weight (counting sort on min(w, 31)), so
@@ -668,7 +728,9 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
             __syncwarp();
             for (int i = lane; i <= rhi; i += 32) runw[i] = 0;
         }
+#if PC_FR_ORDER || !PC_FR_DIET
         __syncthreads();
+#endif
         // ---------------------------------------------------------- runs
         while (nrun > 0) {
             int k = 0;
