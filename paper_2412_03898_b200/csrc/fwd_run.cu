@@ -784,7 +784,9 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                     const unsigned wb = recB[i];
                     const unsigned hm = __ballot_sync(0xffffffffu, (int)(wb & 0xffff) < j0 + FR_RUN &&
                                                                        (int)(wb >> 16) > j0);
-#if PC_FR_DIRECT
+#if PC_FR_DIRECT && PC_FR_DIRECT_MIN < 32
+                // (with the default threshold of 32 the per-group full-run
+                // range above already took every such group)
                 if (__popc(hm) >= PC_FR_DIRECT_MIN) {
                     // (nearly) the whole group meets the run: each lane takes
                     // its own ball directly (no queue round trip); lanes whose
