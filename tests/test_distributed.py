@@ -117,3 +117,33 @@ def test_sharded_gradients_match_single_process(tmp_path, mode):
     assert np.linalg.norm(res["grads"] - full) <= 1e-12 * np.linalg.norm(full)
     assert int(res["coinc"][0]) == (1 << 63) - 2          # MIN over ranks
     assert np.array_equal(res["params"][0], res["params"][1])
+
+
+def test_ball_orders_are_permutations_and_hilbert_has_unit_steps():
+    """engine.hilbert_order (the internal ball layout): a permutation; on a
+    full 2^b lattice consecutive cells are face neighbours (the property the
+    32-ball culling groups rely on), which the Z-order lacks."""
+    from paper_2412_03898_b200.engine import hilbert_order, morton_order
+    g = np.stack(np.meshgrid(np.arange(16), np.arange(16), np.arange(16),
+                             indexing="ij"), -1).reshape(-1, 3).astype(float)
+    for fn in (hilbert_order, morton_order):
+        o = fn(g, bits=4)
+        assert sorted(o.tolist()) == list(range(len(g)))
+    steps = np.abs(np.diff(g[hilbert_order(g, bits=4)], axis=0)).sum(axis=1)
+    assert (steps == 1).all()
+    rng = np.random.default_rng(3)
+    mu = rng.uniform(-20, 20, (5000, 3))
+    o = hilbert_order(mu)
+    assert sorted(o.tolist()) == list(range(5000))
+    ext = lambda order: np.mean(np.ptp(mu[order][:4992].reshape(-1, 32, 3), axis=1).max(axis=1))
+    assert ext(o) <= ext(morton_order(mu))
+    assert len(hilbert_order(np.zeros((0, 3)))) == 0
+    # the engine's layout: Hilbert runs of 128 balls, radius-sorted inside
+    from paper_2412_03898_b200.engine import spatial_ball_order
+    a0 = rng.uniform(0.1, 0.5, 5000)
+    s = spatial_ball_order(mu, a0)
+    assert sorted(s.tolist()) == list(range(5000))
+    for k in range(0, 5000, 128):
+        assert set(s[k:k + 128]) == set(o[k:k + 128])
+        assert (np.diff(a0[s[k:k + 128]]) >= 0).all()
+    assert len(spatial_ball_order(np.zeros((0, 3)), np.zeros(0))) == 0
