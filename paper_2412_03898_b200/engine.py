@@ -119,11 +119,12 @@ def hilbert_order(mu: np.ndarray, bits: int = 10) -> np.ndarray:
 
 def spatial_ball_order(mu: np.ndarray, a0: np.ndarray | None = None) -> np.ndarray:
     """The engine's internal ball layout: Hilbert order of the centres, then,
-    inside every run of `PC_BALL_SEG` (128) consecutive balls, a stable sort
+    inside every run of `PC_BALL_SEG` (64) consecutive balls, a stable sort
     by radius.  Neighbouring balls of equal radius have equal window lengths,
     so the forward's 32-ball groups meet their edge runs together (config 3:
-    25 % fewer partial (group, run) visits) and the four balls of an adjoint
-    CTA finish each sensor block together.  `PC_BALL_ORDER` = `hilbert` (no
+    ~20 % fewer partial (group, run) visits; forward 248.2 -> 242.5 ms,
+    config 4 1370 -> 1317 ms with runs of 128; runs of 128 / 256 cost
+    locality on the sparser config 2).  `PC_BALL_ORDER` = `hilbert` (no
     radius pass) or `morton` (Z-order) select the older layouts."""
     kind = os.environ.get("PC_BALL_ORDER", "hilbert_a0")
     if kind == "morton":
@@ -131,7 +132,7 @@ def spatial_ball_order(mu: np.ndarray, a0: np.ndarray | None = None) -> np.ndarr
     order = hilbert_order(mu)
     if kind == "hilbert" or a0 is None or len(order) == 0:
         return order
-    seg = max(1, int(os.environ.get("PC_BALL_SEG", "128")))
+    seg = max(1, int(os.environ.get("PC_BALL_SEG", "64")))
     a = np.asarray(a0, dtype=np.float64).reshape(-1)[order]
     n = len(order)
     pad = (-n) % seg

@@ -138,12 +138,12 @@ def test_ball_orders_are_permutations_and_hilbert_has_unit_steps():
     ext = lambda order: np.mean(np.ptp(mu[order][:4992].reshape(-1, 32, 3), axis=1).max(axis=1))
     assert ext(o) <= ext(morton_order(mu))
     assert len(hilbert_order(np.zeros((0, 3)))) == 0
-    # the engine's layout: Hilbert runs of 128 balls, radius-sorted inside
+    # the engine's layout: Hilbert runs of 64 balls, radius-sorted inside
     from paper_2412_03898_b200.engine import spatial_ball_order
     a0 = rng.uniform(0.1, 0.5, 5000)
     s = spatial_ball_order(mu, a0)
     assert sorted(s.tolist()) == list(range(5000))
-    for k in range(0, 5000, 128):
-        assert set(s[k:k + 128]) == set(o[k:k + 128])
-        assert (np.diff(a0[s[k:k + 128]]) >= 0).all()
+    for k in range(0, 5000, 64):
+        assert set(s[k:k + 64]) == set(o[k:k + 64])
+        assert (np.diff(a0[s[k:k + 64]]) >= 0).all()
     assert len(spatial_ball_order(np.zeros((0, 3)), np.zeros(0))) == 0
