@@ -884,6 +884,18 @@ constexpr int ADJ_UNROLL = PC_ADJ_UNROLL;
 #ifndef PC_ADJ_LOCKSTEP
 #define PC_ADJ_LOCKSTEP 1
 #endif
+// PC_ADJ_V8 1: the fast sweep reads 8 consecutive residual samples per lane
+// with one 256-bit load (LDG.E.256 on sm_100a): a pair's two lanes cover 64
+// contiguous, 32-byte aligned bytes per request, i.e. exactly one sector per
+// lane, instead of 2 x 16 bytes straddling sectors (23 sectors and ~8 L1
+// data-pipe wavefronts per 128 samples; the L1 data pipe runs at 95 % of its
+// peak).  Windows are extended to multiples of 8 samples.  Measured (config
+// 3): 371.7 ms at ptxas's 72 registers (7 CTAs / SM), 393.8 ms forced to 64
+// (PC_ADJ_MINB=8: register moves and rematerialised constants in the loop)
+// against 367.1 ms: off.
+#ifndef PC_ADJ_V8
+#define PC_ADJ_V8 0
+#endif
 #ifndef PC_ADJ_TMA
 #define PC_ADJ_TMA 0          // > 0: TMA-staged adjoint with that many balls per CTA
 #endif
@@ -915,6 +927,13 @@ __device__ __forceinline__ float4 load_quad(const float* __restrict__ row, int j
     if (ALIGNED) return __ldg(reinterpret_cast<const float4*>(row + j));
     return make_float4(j < T ? __ldg(row + j) : 0.f, j + 1 < T ? __ldg(row + j + 1) : 0.f,
                        j + 2 < T ? __ldg(row + j + 2) : 0.f, j + 3 < T ? __ldg(row + j + 3) : 0.f);
+}
+// Residual samples j .. j+7 with one 256-bit load (32-byte aligned).
+__device__ __forceinline__ void load_oct(const float* __restrict__ p, float4& a, float4& b) {
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                   "=f"(b.w)
+                 : "l"(p));
 }
 __device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
 __device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
@@ -955,8 +974,16 @@ __device__ __forceinline__ void accum_pair_mufu(float2 r, float2 x, float2& A0, 
 // which add their partial G into the zeroed output; with exactly two
 // addends onto 0 the sum is order-independent (IEEE addition commutes), so
 // the result stays deterministic.
+// PC_ADJ_MINB > 0: min-blocks hint of the launch bounds (0: ptxas's own choice)
+#ifndef PC_ADJ_MINB
+#define PC_ADJ_MINB 0
+#endif
 template <bool ALIGNED, bool SPLIT>
+#if PC_ADJ_MINB > 0
+__global__ void __launch_bounds__(ADJ_WARPS * 32, PC_ADJ_MINB) k_adjoint(AdjArgs a) {
+#else
 __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
+#endif
     __shared__ __align__(16) float4 recs[ADJ_WARPS][32][3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = (int64_t)blockIdx.x * ADJ_WARPS + warp;
@@ -1044,11 +1071,41 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             int j = (jl & ~3) + 4 * sub;
             const float* row = rblk + (size_t)pi * T;
             float2 A0 = splat2(0.f), A1 = A0, A2 = A0, A3 = A0;
-            if (j < je1) {
+            bool swept = false;
+#if PC_ADJ_V8
+            static_assert(PC_ADJ_MODE == 2 && LG == 2, "PC_ADJ_V8: MUFU sweep, two lanes per pair");
+            if (ALIGNED && fast && !near) {
+                // octs j8, j8 + 16, ... of the window extended to multiples of 8
+                const int je8 = (jh + 7) & ~7;
+                const int j8 = (jl & ~7) + 8 * sub;
+                if (j8 < je8) {
+                    const int jrr = __float_as_int(r0.y);
+                    const float2 k = make_float2((float)(j8 - jrr), (float)(j8 + 1 - jrr));
+                    float2 xa = ffma2(k, mvs2, splat2(r0.z));
+                    float2 xb = ffma2(fadd2(k, splat2(2.f)), mvs2, splat2(r0.z));
+                    const float2 s1 = splat2(-4.f * vs), s2 = splat2(-12.f * vs);
+                    const float* p = row + j8;
+                    for (int n = (je8 - j8 + 15) >> 4; n > 0; --n, p += 16) {
+                        float4 q0, q1;
+                        load_oct(p, q0, q1);
+                        accum_pair_mufu(lo2(q0), xa, A0, A1, A2, A3);
+                        accum_pair_mufu(hi2(q0), xb, A0, A1, A2, A3);
+                        xa = fadd2(xa, s1);
+                        xb = fadd2(xb, s1);
+                        accum_pair_mufu(lo2(q1), xa, A0, A1, A2, A3);
+                        accum_pair_mufu(hi2(q1), xb, A0, A1, A2, A3);
+                        xa = fadd2(xa, s2);
+                        xb = fadd2(xb, s2);
+                    }
+                }
+                swept = true;
+            }
+#endif
+            if (!swept && j < je1) {
                 const int jrr = __float_as_int(r0.y);
                 float2 k = make_float2((float)(j - jrr), (float)(j + 1 - jrr));
                 const float2 two = splat2(2.f);
-                if (fast && !near) {
+                if (fast && !near && !(PC_ADJ_V8 && ALIGNED)) {
                     // two chains per lane: samples (j, j+1) and (j+2, j+3)
                     float2 xa = ffma2(k, mvs2, splat2(r0.z));
                     float2 xb = ffma2(fadd2(k, two), mvs2, splat2(r0.z));
@@ -1816,7 +1873,11 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     const int64_t ctas = (int64_t)grid.x * n_frames;
     const bool split = adj_split() > 0 && a.M >= 64 && ctas < (int64_t)adj_split() * 8 * num_sms();
     a.msplit = ((a.M / 2 + 31) / 32) * 32;
+#if PC_ADJ_V8
+    const bool aligned = array->n_samples % 8 == 0 && reinterpret_cast<uintptr_t>(residual) % 32 == 0;
+#else
     const bool aligned = array->n_samples % 4 == 0 && reinterpret_cast<uintptr_t>(residual) % 16 == 0;
+#endif
     if (split) {
         if (cudaMemsetAsync(G, 0, (size_t)n_balls * n_frames * 5 * sizeof(float), st) != cudaSuccess)
             return PC_ERR_CUDA;
