@@ -64,8 +64,18 @@ namespace PC_FR_NS {
 #ifndef PC_FR_DIRECT
 #define PC_FR_DIRECT 1
 #endif
+// a partly-hit group with at least this many members on the run is swept
+// directly (lane = ball, the other lanes idle) instead of through the queue
+// (config 3 forward, radius-sorted layout: 32 / 28 / 24 / 16 -> 242.3 /
+// 240.6 / 240.6 / 243.1 ms)
 #ifndef PC_FR_DIRECT_MIN
-#define PC_FR_DIRECT_MIN 32
+#define PC_FR_DIRECT_MIN 24
+#endif
+// PC_FR_QDUMMY 1 (default): the queue push is an unconditional store
+// (non-members write a per-lane dummy slot behind the queue) instead of a
+// branch (config 3 forward 240.6 -> 239.7 ms, bit-identical)
+#ifndef PC_FR_QDUMMY
+#define PC_FR_QDUMMY 1
 #endif
 #ifndef PC_FR_CHAIN1
 #define PC_FR_CHAIN1 0
@@ -190,7 +200,7 @@ struct FrSmem {
     static constexpr size_t gspan = recY + (size_t)FR_CHUNK * 4;         // u32 [C/32]
     static constexpr size_t gfull = gspan + (size_t)FR_GROUPS * 4;       // u32 [C/32]: runs every member meets
     static constexpr size_t queue = gfull + (size_t)FR_GROUPS * 4;       // u16 [W][QLEN]
-    static constexpr size_t xbuf = queue + (size_t)FR_WARPS * FR_QLEN * 2;   // f32 [W][32][XPAD]
+    static constexpr size_t xbuf = queue + (size_t)FR_WARPS * (FR_QLEN + 32 * PC_FR_QDUMMY) * 2;   // f32 [W][32][XPAD]
     static constexpr size_t ctl = xbuf + (size_t)FR_WARPS * 32 * FR_XPAD * 4; // int [8]
     // TMA stage of the next chunk's raw balls: mu f64 [C][3] | a0 f32 [C] | p0 f32 [C]
     static constexpr size_t rawmu = ctl + 64;
@@ -528,7 +538,7 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
     __syncthreads();
 #endif
     const unsigned lt = (1u << lane) - 1u;
-    unsigned short* Q = queue + warp * FR_QLEN;
+    unsigned short* Q = queue + warp * (FR_QLEN + 32 * PC_FR_QDUMMY);
     float* xb = xbuf + warp * 32 * FR_XPAD;
     int par = 0;
     for (int64_t c0 = 0; c0 < a.B; c0 += FR_CHUNK, par ^= 1) {
@@ -806,7 +816,12 @@ __global__ void __launch_bounds__(FR_THREADS, PC_FR_MINB) k_fwd_run(FwdRunArgs a
                     continue;
                 }
 #endif
+#if PC_FR_QDUMMY
+                    Q[((hm >> lane) & 1u) ? ((qn + __popc(hm & lt)) & (FR_QLEN - 1)) : FR_QLEN + lane] =
+                        (unsigned short)i;
+#else
                     if ((hm >> lane) & 1u) Q[(qn + __popc(hm & lt)) & (FR_QLEN - 1)] = (unsigned short)i;
+#endif
                     qn += __popc(hm);
                     if (qn - qd >= 32) {
                         __syncwarp();

@@ -919,7 +919,54 @@ struct AdjArgs {
     ArrayConsts ac;
     int msplit;     // SPLIT: first sensor of the second half (multiple of 32)
     long long fo, so, mt; // coincidence word: frame offset, sensor offset, total sensors
+    // PC_ADJ_DIET: the float forms of the array constants pair_setup converts
+    // per pair (bit-identical values, formed once on the host)
+    float inv_v_f, t0_f, inv_dt_f, sa_f, vt0_f, vdt_f;
+    double vdt_d, vt0_d;
 };
+
+#ifndef PC_ADJ_DIET
+#define PC_ADJ_DIET 0
+#endif
+#if PC_ADJ_DIET
+// pair_setup (common.cuh) for the adjoint with the constants above, the raw
+// MUFU rsqrt (R^2 is a normal float wherever the result is used) and the
+// reciprocal of R from one fp64 Newton step on that estimate instead of an
+// fp64 division (relative error ~1e-13).
+__device__ __forceinline__ void adj_pair_setup(double dx, double dy, double dz, float a0, float s,
+                                               const AdjArgs& a, PairSetup& q, double& inv_r) {
+    const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const float r2f = (float)R2;
+    float rinv;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(r2f));
+    const float rf = r2f * rinv;
+    const double rid = (double)rinv;
+    const double R = r2f > 1e-30f ? fma(fma(-(double)rf, (double)rf, R2), 0.5 * rid, (double)rf)
+                                  : sqrt(R2);
+    q.R = R;
+    inv_r = r2f > 1e-30f ? rid * fma(-R, rid, 2.0) : 1.0 / R;
+    inv_r = inv_r * fma(-R, inv_r, 2.0);
+    const int T = a.ac.T;
+    int lo, hi;
+    const float tc = ((float)R * a.inv_v_f - a.t0_f) * a.inv_dt_f;
+    if (a.ac.exact) {
+        lo = 0;
+        hi = T;
+    } else {
+        const float sa = a.sa_f * a0;
+        lo = (int)fminf(fmaxf(ceilf(tc - sa), 0.f), (float)T);
+        hi = (int)fminf(fmaxf(floorf(tc + sa) + 1.f, 0.f), (float)T);
+    }
+    q.jl = max(lo, 0);
+    q.jh = min(hi, T);
+    const int rc = __float2int_rn(tc);
+    q.jr = min(max(rc, q.jl), max(q.jh - 1, q.jl));
+    const double vt = fma((double)q.jr, a.vdt_d, a.vt0_d);
+    q.X = (float)(R - vt) * s;
+    q.Y = (float)(R + vt) * s;
+    q.near = (float)R + a.vt0_f + a.vdt_f * (float)q.jl < 10.f * a0;
+}
+#endif
 
 // Residual samples j .. j+3 (one 16-byte load when rows are 16-byte aligned).
 template <bool ALIGNED>
@@ -1031,7 +1078,12 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             const double dy = my - a.pos[3 * m + 1];
             const double dz = mz - a.pos[3 * m + 2];
             PairSetup q;
+#if PC_ADJ_DIET
+            double ir;
+            adj_pair_setup(dx, dy, dz, av, s, a, q, ir);
+#else
             pair_setup(dx, dy, dz, av, s, a.ac, 0, T, q);
+#endif
             if (q.R < kCoincidenceEps) {
                 atomicMin(a.coinc, ((a.fo + f) * a.B + b) * a.mt + a.so + m);
             } else if (q.jh > q.jl) {
@@ -1040,7 +1092,9 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
                 jr = q.jr;
                 X = q.X;
                 Y = q.Y;
+#if !PC_ADJ_DIET
                 const double ir = 1.0 / q.R;
+#endif
                 const float inv2R = (float)(0.5 * ir);
                 kp = inv2R * inv_s;
                 ka = ka_ball * inv2R;
@@ -1848,6 +1902,14 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     a.F = n_frames;
     a.M = array->n_sensors;
     a.ac = ac;
+    a.inv_v_f = (float)ac.inv_v;
+    a.t0_f = (float)ac.t0;
+    a.inv_dt_f = (float)ac.inv_dt;
+    a.sa_f = (float)(ac.support * ac.inv_v * ac.inv_dt);
+    a.vt0_f = (float)(ac.v * ac.t0);
+    a.vdt_f = (float)(ac.v * ac.dt);
+    a.vdt_d = ac.v * ac.dt;
+    a.vt0_d = ac.v * ac.t0;
     dim3 grid((unsigned)((n_balls + ADJ_WARPS - 1) / ADJ_WARPS), n_frames);
     cudaStream_t st = as_stream(stream);
 #if PC_ADJ_TMA
