@@ -896,6 +896,13 @@ constexpr int ADJ_UNROLL = PC_ADJ_UNROLL;
 #ifndef PC_ADJ_V8
 #define PC_ADJ_V8 0
 #endif
+// PC_ADJ_PTR 1 (default): the aligned fast sweep runs on one pointer (chunks
+// of 2 quads, a single-quad remainder) instead of carrying the sample index
+// through the loop: one loop-control instruction less and 56 registers
+// instead of 64 (9 CTAs / SM); config 3 adjoint 361.6 -> 355.7 ms.
+#ifndef PC_ADJ_PTR
+#define PC_ADJ_PTR 1
+#endif
 #ifndef PC_ADJ_TMA
 #define PC_ADJ_TMA 0          // > 0: TMA-staged adjoint with that many balls per CTA
 #endif
@@ -1193,6 +1200,23 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     accum_pair_mufu(hi2(R), xb, A0, A1, A2, A3);         \
     xa = fadd2(xa, mD2);                                 \
     xb = fadd2(xb, mD2);
+#endif
+#if PC_ADJ_PTR
+                    if (ALIGNED) {
+                        // the same sweep on one running pointer (no sample index
+                        // carried through the loop)
+                        const float4* p4 = reinterpret_cast<const float4*>(row + j);
+                        for (; n >= 2; n -= 2, p4 += 2 * (LSTRIDE / 4)) {
+                            const float4 ra = __ldg(p4), rb = __ldg(p4 + LSTRIDE / 4);
+                            PC_ADJ_STEP(ra)
+                            PC_ADJ_STEP(rb)
+                        }
+                        if (n > 0) {
+                            const float4 ra = __ldg(p4);
+                            PC_ADJ_STEP(ra)
+                        }
+                        n = 0;
+                    }
 #endif
                     // chunks of ADJ_CHUNK quads: that many loads in flight
 #pragma unroll ADJ_UNROLL
