@@ -892,7 +892,8 @@ constexpr int ADJ_UNROLL = PC_ADJ_UNROLL;
 // peak).  Windows are extended to multiples of 8 samples.  Measured (config
 // 3): 371.7 ms at ptxas's 72 registers (7 CTAs / SM), 393.8 ms forced to 64
 // (PC_ADJ_MINB=8: register moves and rematerialised constants in the loop)
-// against 367.1 ms: off.
+// against 367.1 ms; against the later pointer sweep (356.1 ms at 56
+// registers) 388.6 ms at ptxas's 78 and 376.6 ms forced to 56: off.
 #ifndef PC_ADJ_V8
 #define PC_ADJ_V8 0
 #endif
