@@ -897,6 +897,21 @@ constexpr int ADJ_UNROLL = PC_ADJ_UNROLL;
 #ifndef PC_ADJ_V8
 #define PC_ADJ_V8 0
 #endif
+// PC_ADJ_ALIGN8 1 (default): aligned fast sweeps start on a 32-byte boundary,
+// so the two lanes' quads of a pair share one sector in every request (16
+// instead of ~23 sectors per 16-pair request; at most one more quad at the
+// window start, weights < exp(-18)).  The L1 data pipe was at 97 % of its
+// peak: config 3 adjoint 356.3 -> 343.6 ms, config 2 4.71 -> 4.55 ms.
+#ifndef PC_ADJ_ALIGN8
+#define PC_ADJ_ALIGN8 1
+#endif
+// PC_ADJ_COLD 1 (default): the per-ball values only the pair setup needs
+// (centre, a0, p0, scale factors) are parked in shared memory instead of
+// living in 11 registers through the sweeps: 48 instead of 56 registers
+// (10 CTAs / SM), config 3 adjoint 343.6 -> 341.8 ms.
+#ifndef PC_ADJ_COLD
+#define PC_ADJ_COLD 1
+#endif
 // PC_ADJ_PTR 1 (default): the aligned fast sweep runs on one pointer (chunks
 // of 2 quads, a single-quad remainder) instead of carrying the sample index
 // through the loop: one loop-control instruction less and 56 registers
@@ -1072,6 +1087,23 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f;
     float4(&rec)[32][3] = recs[warp];
     const int grp = lane / LG, sub = lane % LG;
+#if PC_ADJ_COLD
+    __shared__ double cold_d[ADJ_WARPS][4];
+    __shared__ float cold_f[ADJ_WARPS][8];
+    if (lane == 0) {
+        cold_d[warp][0] = mx;
+        cold_d[warp][1] = my;
+        cold_d[warp][2] = mz;
+        cold_f[warp][0] = av;
+        cold_f[warp][1] = pv;
+        cold_f[warp][2] = s;
+        cold_f[warp][3] = inv_s;
+        cold_f[warp][4] = ka_ball;
+    }
+    __syncwarp();
+    const volatile double* cd = cold_d[warp];
+    const volatile float* cf = cold_f[warp];
+#endif
 
     const float* rblk = a.resid + ((size_t)f * a.M + m_lo) * T;   // this block's first row
     for (int mb = m_lo; mb < m_hi; mb += 32, rblk += (size_t)32 * T) {
@@ -1084,15 +1116,22 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
 #else
         if (m < a.M) {
 #endif
-            const double dx = mx - a.pos[3 * m + 0];
-            const double dy = my - a.pos[3 * m + 1];
-            const double dz = mz - a.pos[3 * m + 2];
+#if PC_ADJ_COLD
+            const double bx = cd[0], by = cd[1], bz = cd[2];
+            const float b_av = cf[0], b_pv = cf[1], b_s = cf[2], b_inv_s = cf[3], b_ka = cf[4];
+#else
+            const double bx = mx, by = my, bz = mz;
+            const float b_av = av, b_pv = pv, b_s = s, b_inv_s = inv_s, b_ka = ka_ball;
+#endif
+            const double dx = bx - a.pos[3 * m + 0];
+            const double dy = by - a.pos[3 * m + 1];
+            const double dz = bz - a.pos[3 * m + 2];
             PairSetup q;
 #if PC_ADJ_DIET
             double ir;
-            adj_pair_setup(dx, dy, dz, av, s, a, q, ir);
+            adj_pair_setup(dx, dy, dz, b_av, b_s, a, q, ir);
 #else
-            pair_setup(dx, dy, dz, av, s, a.ac, 0, T, q);
+            pair_setup(dx, dy, dz, b_av, b_s, a.ac, 0, T, q);
 #endif
             if (q.R < kCoincidenceEps) {
                 atomicMin(a.coinc, ((a.fo + f) * a.B + b) * a.mt + a.so + m);
@@ -1106,10 +1145,10 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
                 const double ir = 1.0 / q.R;
 #endif
                 const float inv2R = (float)(0.5 * ir);
-                kp = inv2R * inv_s;
-                ka = ka_ball * inv2R;
-                kR2 = pv * inv2R;
-                kR1 = -kR2 * (float)ir * inv_s;
+                kp = inv2R * b_inv_s;
+                ka = b_ka * inv2R;
+                kR2 = b_pv * inv2R;
+                kR1 = -kR2 * (float)ir * b_inv_s;
                 ux = (float)(dx * ir);
                 uy = (float)(dy * ir);
                 uz = (float)(dz * ir);
@@ -1132,7 +1171,11 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
             // window extended to multiples of 4 (the extra samples weigh
             // < exp(-19) of the peak); lane `sub` takes quads j, j + 16, ...
             const int je1 = (jh + 3) & ~3;
+#if PC_ADJ_ALIGN8
+            int j = ((ALIGNED && fast && !near) ? (jl & ~7) : (jl & ~3)) + 4 * sub;
+#else
             int j = (jl & ~3) + 4 * sub;
+#endif
             const float* row = rblk + (size_t)pi * T;
             float2 A0 = splat2(0.f), A1 = A0, A2 = A0, A3 = A0;
             bool swept = false;
