@@ -912,6 +912,17 @@ constexpr int ADJ_UNROLL = PC_ADJ_UNROLL;
 #ifndef PC_ADJ_COLD
 #define PC_ADJ_COLD 1
 #endif
+// PC_ADJ_B2 = NB in {2, 4, 8, 16}: a warp owns NB neighbouring balls and walks the
+// sensors 32 / NB at a time; its 32 pair records interleave the balls per
+// sensor, so the 16 pairs of a request cover 16 / NB residual rows (the
+// balls' windows in a row overlap) instead of 16: fewer distinct L1 lines
+// per request.  0: one ball per warp.  Config 3 adjoint, NB = 0 / 2 / 4:
+// 343.6 / 332.3 / 333.7 ms (config 2: 4.56 / 4.50 / 4.71): 2 is the default.
+#ifndef PC_ADJ_B2
+#define PC_ADJ_B2 2
+#endif
+constexpr int ADJ_NB = PC_ADJ_B2 > 0 ? PC_ADJ_B2 : 1;      // balls per warp
+constexpr int ADJ_NBSH = ADJ_NB == 16 ? 4 : ADJ_NB == 8 ? 3 : ADJ_NB == 4 ? 2 : ADJ_NB == 2 ? 1 : 0;
 // PC_ADJ_PTR 1 (default): the aligned fast sweep runs on one pointer (chunks
 // of 2 quads, a single-quad remainder) instead of carrying the sample index
 // through the loop: one loop-control instruction less and 56 registers
@@ -1058,7 +1069,18 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
 #endif
     __shared__ __align__(16) float4 recs[ADJ_WARPS][32][3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if PC_ADJ_B2
+    static_assert(PC_ADJ_COLD && PC_ADJ_LOCKSTEP && PC_ADJ_MODE == 2 && LG == 2 && !PC_ADJ_V8,
+                  "PC_ADJ_B2 is written for the default sweep");
+    static_assert(ADJ_NB == 2 || ADJ_NB == 4 || ADJ_NB == 8 || ADJ_NB == 16,
+                  "PC_ADJ_B2: 2, 4, 8 or 16 balls per warp");
+    // setup lanes: ball = lane % NB; sweep lanes (pair = lane / 2): ball = (lane / 2) % NB
+    const int64_t b0 = ((int64_t)blockIdx.x * ADJ_WARPS + warp) * ADJ_NB;
+    const int64_t b = b0 + (lane & (ADJ_NB - 1));
+    const int64_t b_swp = b0 + ((lane >> 1) & (ADJ_NB - 1));
+#else
     const int64_t b = (int64_t)blockIdx.x * ADJ_WARPS + warp;
+#endif
     const int f = SPLIT ? (int)(blockIdx.y >> 1) : (int)blockIdx.y;
     const int m_lo = SPLIT ? (int)(blockIdx.y & 1) * a.msplit : 0;
     const int m_hi = SPLIT ? ((blockIdx.y & 1) ? a.M : min(a.M, a.msplit)) : a.M;
@@ -1072,7 +1094,13 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     const double mx = a.mu[3 * sb + 0], my = a.mu[3 * sb + 1], mz = a.mu[3 * sb + 2];
     const float av = a.a0[sb], pv = a.p0[sb];
     const float s = scale_of(av);
+#if PC_ADJ_B2
+    const bool live_swp = b_swp < a.B;
+    const size_t sb_swp = (size_t)f * a.B + (live_swp ? b_swp : a.B - 1);
+    const float vs = a.ac.vdt * scale_of(a.a0[sb_swp]);   // the sweep ball's sample step
+#else
     const float vs = a.ac.vdt * s;
+#endif
     const float inv_s = 1.f / s;
     const float ka_ball = pv / (av * av * av) * inv_s * inv_s * inv_s;
     const int T = a.ac.T;
@@ -1088,26 +1116,39 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     float4(&rec)[32][3] = recs[warp];
     const int grp = lane / LG, sub = lane % LG;
 #if PC_ADJ_COLD
+#if PC_ADJ_B2
+    __shared__ double cold_d[ADJ_NB * ADJ_WARPS][4];
+    __shared__ float cold_f[ADJ_NB * ADJ_WARPS][8];
+    const int cw = ADJ_NB * warp + (lane & (ADJ_NB - 1));
+    if (lane < ADJ_NB) {
+#else
     __shared__ double cold_d[ADJ_WARPS][4];
     __shared__ float cold_f[ADJ_WARPS][8];
+    const int cw = warp;
     if (lane == 0) {
-        cold_d[warp][0] = mx;
-        cold_d[warp][1] = my;
-        cold_d[warp][2] = mz;
-        cold_f[warp][0] = av;
-        cold_f[warp][1] = pv;
-        cold_f[warp][2] = s;
-        cold_f[warp][3] = inv_s;
-        cold_f[warp][4] = ka_ball;
+#endif
+        cold_d[cw][0] = mx;
+        cold_d[cw][1] = my;
+        cold_d[cw][2] = mz;
+        cold_f[cw][0] = av;
+        cold_f[cw][1] = pv;
+        cold_f[cw][2] = s;
+        cold_f[cw][3] = inv_s;
+        cold_f[cw][4] = ka_ball;
     }
     __syncwarp();
-    const volatile double* cd = cold_d[warp];
-    const volatile float* cf = cold_f[warp];
+    const volatile double* cd = cold_d[cw];
+    const volatile float* cf = cold_f[cw];
 #endif
 
     const float* rblk = a.resid + ((size_t)f * a.M + m_lo) * T;   // this block's first row
+#if PC_ADJ_B2
+    for (int mb = m_lo; mb < m_hi; mb += 32 / ADJ_NB, rblk += (size_t)(32 / ADJ_NB) * T) {
+        const int m = mb + (lane >> ADJ_NBSH);
+#else
     for (int mb = m_lo; mb < m_hi; mb += 32, rblk += (size_t)32 * T) {
         const int m = mb + lane;
+#endif
         int win = -1, wh = 0, jr = 0;           // window [jl, jh) (win = jl | near << 30)
         float X = 0.f, Y = 0.f, kp = 0.f, ka = 0.f, kR1 = 0.f, kR2 = 0.f;
         float ux = 0.f, uy = 0.f, uz = 0.f;
@@ -1158,7 +1199,11 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
         rec[lane][1] = make_float4(ka, kR1, kR2, ux);
         rec[lane][2] = make_float4(uy, uz, Y, __int_as_float(wh));
         __syncwarp();
+#if PC_ADJ_B2
+        const int npair = min(32, ADJ_NB * (m_hi - mb));
+#else
         const int npair = min(32, m_hi - mb);
+#endif
         for (int pb = 0; pb < npair; pb += NGRP) {
             const int pi = pb + grp;
             if (pi >= npair) continue;
@@ -1176,7 +1221,11 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
 #else
             int j = (jl & ~3) + 4 * sub;
 #endif
+#if PC_ADJ_B2
+            const float* row = rblk + (size_t)(pi >> ADJ_NBSH) * T;
+#else
             const float* row = rblk + (size_t)pi * T;
+#endif
             float2 A0 = splat2(0.f), A1 = A0, A2 = A0, A3 = A0;
             bool swept = false;
 #if PC_ADJ_V8
@@ -1336,6 +1385,21 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
         __syncthreads();   // the CTA's balls read the same sensor rows together
 #endif
     }
+#if PC_ADJ_B2
+    // lanes with equal (lane / 2) % NB hold one ball's partials: fixed xor
+    // order over the other lane bits
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        if (o >= 2 && o < 2 * ADJ_NB) continue;
+        g0 += __shfl_xor_sync(0xffffffffu, g0, o);
+        g1 += __shfl_xor_sync(0xffffffffu, g1, o);
+        g2 += __shfl_xor_sync(0xffffffffu, g2, o);
+        g3 += __shfl_xor_sync(0xffffffffu, g3, o);
+        g4 += __shfl_xor_sync(0xffffffffu, g4, o);
+    }
+    if ((lane & ~(2 * (ADJ_NB - 1))) == 0 && live_swp) {
+        float* out = a.G + 5 * sb_swp;
+#else
 #if PC_ADJ_LOCKSTEP
     if (!live) return;
 #endif
@@ -1346,6 +1410,7 @@ __global__ void __launch_bounds__(ADJ_WARPS * 32) k_adjoint(AdjArgs a) {
     g4 = warp_sum(g4);
     if (lane == 0) {
         float* out = a.G + 5 * sb;
+#endif
         if (SPLIT) {
             atomicAdd(out + 0, g0);
             atomicAdd(out + 1, g1);
@@ -1980,7 +2045,11 @@ extern "C" int pc_residual_state_grads(const double* mu_t, const float* a0_t, co
     a.vdt_f = (float)(ac.v * ac.dt);
     a.vdt_d = ac.v * ac.dt;
     a.vt0_d = ac.v * ac.t0;
+#if PC_ADJ_B2
+    dim3 grid((unsigned)((n_balls + ADJ_NB * ADJ_WARPS - 1) / (ADJ_NB * ADJ_WARPS)), n_frames);
+#else
     dim3 grid((unsigned)((n_balls + ADJ_WARPS - 1) / ADJ_WARPS), n_frames);
+#endif
     cudaStream_t st = as_stream(stream);
 #if PC_ADJ_TMA
     if (!ac.exact && array->n_samples % 4 == 0 &&
