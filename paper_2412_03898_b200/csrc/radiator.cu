@@ -850,18 +850,21 @@ __global__ void __launch_bounds__(256) k_loss_reduce(const double* __restrict__ 
 
 // ---------------------------------------------------------------- adjoint
 //
-// One warp owns one (ball, frame).  Per block of 32 sensors the lanes form the
-// pair setups in parallel (fp64) into 48-byte shared-memory records; then
-// lane groups of LG lanes take one pair each (NGRP pairs at a time).  Each
-// lane owns sample pairs (j, j+1) of the pair's even-extended window, reads
-// them with one 64-bit load and accumulates three scaled partial sums with
-// packed fp32x2 arithmetic:
-//   A1 = sum r e x,  AQ = sum r e (1 - kappa x^2),  A3 = sum r e x^3,
-// e = 2^-x^2 from the recurrence e <- e g, g <- g h (MUFU only at the start;
+// One warp owns two neighbouring balls of one frame (PC_ADJ_B2; one ball
+// with PC_ADJ_B2=0).  Per block of 16 sensors the lanes form the 32 pair
+// setups in parallel (fp64; lane = 2 * sensor + ball) into 48-byte
+// shared-memory records; then lane groups of LG lanes take one pair each
+// (NGRP = 16 pairs at a time: 8 sensors x 2 balls, i.e. 8 residual rows per
+// load request).  Each lane owns quads (j .. j+3) of the pair's window
+// (started on a 32-byte boundary, PC_ADJ_ALIGN8), reads them with one
+// 128-bit load and accumulates the moments
+//   A0 = sum r e,  A1 = sum r e x,  A2 = sum r e x^2,  A3 = sum r e x^3
+// (AQ = A0 - kappa A2) with packed fp32x2 arithmetic, e = 2^-x^2 from MUFU
+// (PC_ADJ_MODE 2; modes 0 / 1 step it by the recurrence e <- e g, g <- g h;
 // the near-field and exact paths use one MUFU per term and sample).  Every
 // pair constant multiplies a lane-local partial, so the per-pair reduction is
-// deferred: lanes fold their partials into five ball accumulators and the
-// warp reduces once per ball (fixed xor order: deterministic).
+// deferred: lanes fold their partials into five ball accumulators and each
+// ball's lanes reduce once at the end (fixed xor order: deterministic).
 
 #ifndef PC_ADJ_WARPS
 #define PC_ADJ_WARPS 4
