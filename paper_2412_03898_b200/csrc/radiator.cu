@@ -856,8 +856,8 @@ __global__ void __launch_bounds__(256) k_loss_reduce(const double* __restrict__ 
 // shared-memory records; then lane groups of LG lanes take one pair each
 // (NGRP = 16 pairs at a time: 8 sensors x 2 balls, i.e. 8 residual rows per
 // load request).  Each lane owns quads (j .. j+3) of the pair's window
-// (started on a 32-byte boundary, PC_ADJ_ALIGN8), reads them with one
-// 128-bit load and accumulates the moments
+// (extended to multiples of 4 samples), reads them with one 128-bit load and
+// accumulates the moments
 //   A0 = sum r e,  A1 = sum r e x,  A2 = sum r e x^2,  A3 = sum r e x^3
 // (AQ = A0 - kappa A2) with packed fp32x2 arithmetic, e = 2^-x^2 from MUFU
 // (PC_ADJ_MODE 2; modes 0 / 1 step it by the recurrence e <- e g, g <- g h;
@@ -900,13 +900,15 @@ constexpr int ADJ_UNROLL = PC_ADJ_UNROLL;
 #ifndef PC_ADJ_V8
 #define PC_ADJ_V8 0
 #endif
-// PC_ADJ_ALIGN8 1 (default): aligned fast sweeps start on a 32-byte boundary,
-// so the two lanes' quads of a pair share one sector in every request (16
-// instead of ~23 sectors per 16-pair request; at most one more quad at the
-// window start, weights < exp(-18)).  The L1 data pipe was at 97 % of its
-// peak: config 3 adjoint 356.3 -> 343.6 ms, config 2 4.71 -> 4.55 ms.
+// PC_ADJ_ALIGN8 1: aligned fast sweeps start on a 32-byte boundary, so the
+// two lanes' quads of a pair share one sector in every request (16 instead
+// of ~23 sectors per 16-pair request; at most one more quad at the window
+// start, weights < exp(-18)).  With one ball per warp the L1 data pipe was at
+// 97 % of its peak and this paid (config 3 adjoint 356.3 -> 343.6 ms); with
+// two balls per warp (PC_ADJ_B2, L1 pipe 74 %) the extra quad costs more
+// than the sectors save (336.1 with, 327.5 ms without): off.
 #ifndef PC_ADJ_ALIGN8
-#define PC_ADJ_ALIGN8 1
+#define PC_ADJ_ALIGN8 0
 #endif
 // PC_ADJ_COLD 1 (default): the per-ball values only the pair setup needs
 // (centre, a0, p0, scale factors) are parked in shared memory instead of
